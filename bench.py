@@ -1,0 +1,405 @@
+"""bench.py — SparVAR hot path on B200: last-scale block-sparse attention ms/layer.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference] [--config 8b|2b]
+    python -m torch.distributed.run --nnodes=1 --nproc-per-node N --master-addr 127.0.0.1 \
+        --master-port P bench.py --gpus N ...
+
+Workload (N=1): Infinity-8B-shaped last scale (BASELINE.json configs[3]): schedule 1..64
+(13 scales, q 4096 x kv 10521), decision scale S=11, block 128, head_dim 128, batch 4 x 24 heads
+= 96 (b,h) units, bf16.  N>1: weak scaling, every rank runs its own 96 units (global batch 4N,
+(batch x head) sharding, no data-path collective).
+
+One step = one pass of the whole hot path:
+    a1 local_mask(13) | a2+a3 predict_pattern(S=11, top-5) | a4 map_indices(11->13)
+    a5 build_block_lists for the CSLA layer (sink+local) and the CS4A layer (sink+mapped)
+    a6 block_sparse_attn for the CSLA layer and for the CS4A layer
+`value` = ms per layer = step time / 2 (two attention layers per step, pattern work included).
+The dense sm_100a kernel on the same shape (a7) is timed separately for the speed-up.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "last-scale block-sparse attn ms/layer, tensor-pipe util; x vs own dense sm_100a"
+SIDES = [1, 2, 4, 6, 8, 12, 16, 20, 24, 32, 40, 48, 64]
+CONFIGS = {
+    "8b": dict(name="infinity8b_last_scale", batch=4, heads=24),
+    "2b": dict(name="infinity2b_last_scale", batch=1, heads=16),
+}
+K_T, S_D, BLOCK, D, SINK, WINDOWS, TOPK = 13, 11, 128, 128, 5, (7, 5, 3, 1, 1), 5
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=20)
+    p.add_argument("--warmup", type=int, default=5)
+    p.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    p.add_argument("--config", default="8b", choices=list(CONFIGS))
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    return p.parse_args()
+
+
+# ----------------------------------------------------------------------------- clocks
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index, self.rows, self.proc = index, [], None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.th = threading.Thread(target=self._read, daemon=True)
+            self.th.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) == 6:
+                self.rows.append(parts)
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(2)
+        except Exception:
+            self.proc.kill()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        reasons = sorted({n for r in self.rows for n, v in zip(names, r[2:]) if v == "Active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+# ----------------------------------------------------------------------------- helpers
+def peaks():
+    try:
+        return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))), "measured"
+    except Exception:
+        return {"bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0, "hbm_gbs": 6650.0}, "fallback"
+
+
+def algorithmic_flops(lists, n_q, n_kv, B, Dh):
+    """4*D*sum over active (u,v) of |u|*|v| over real tokens."""
+    tot = 0
+    for u, l in enumerate(lists):
+        qu = min((u + 1) * B, n_q) - u * B
+        for v in l:
+            tot += qu * (min((int(v) + 1) * B, n_kv) - int(v) * B)
+    return 4 * Dh * tot
+
+
+def traffic_from_profile(kernel="attn_fwd_kernel"):
+    p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    try:
+        d = json.load(open(p))
+        return d.get(kernel)
+    except Exception:
+        return None
+
+
+# ----------------------------------------------------------------------------- CPU oracle
+def oracle_sample(seed, bh_global, budget_s=12.0, max_heads=8):
+    """Time the fp64 oracle on a bounded sample of the workload: the CSLA mask (shared by all
+    heads) plus predictor, mapping, list merge and both block-sparse attentions for as many (b,h)
+    units as fit in ~budget_s.  Returns (ms per layer extrapolated to all units, sample text)."""
+    import numpy as np
+    from oracle.attention import block_sparse, merge_lists
+    from oracle.csla import local_block_mask
+    from oracle.geometry import Schedule
+    from oracle.mapping import map_pattern
+    from oracle.predictor import predict_pattern
+    from synth import kv_cache_iid, q_iid
+
+    sched = Schedule(SIDES)
+    t0 = time.perf_counter()
+    local = local_block_mask(sched, K_T, BLOCK, SINK, WINDOWS)
+    t_mask = time.perf_counter() - t0
+    per_head, n = 0.0, 0
+    while n < max_heads and (n == 0 or (t_mask + per_head) < budget_s):
+        b = bh_global + n
+        q = q_iid(seed, K_T, b, 1, sched.N(K_T), D)[0].double().numpy()
+        qs = q_iid(seed, S_D, b, 1, sched.N(S_D), D)[0].double().numpy()
+        k, v = kv_cache_iid(seed, b, 1, sched.C(K_T), D)
+        k, v = k[0].double().numpy(), v[0].double().numpy()
+        t1 = time.perf_counter()
+        src, _ = predict_pattern(qs, k, sched, S_D, BLOCK, SINK, "topk", TOPK)
+        mapped = map_pattern(src, sched, S_D, K_T, BLOCK, SINK, "footprint")
+        block_sparse(q, k, v, sched.C(K_T), BLOCK, merge_lists([local]))
+        block_sparse(q, k, v, sched.C(K_T), BLOCK, merge_lists([mapped]))
+        per_head += time.perf_counter() - t1
+        n += 1
+    return t_mask, per_head / n, n
+
+
+def cpu_cores():
+    try:
+        from threadpoolctl import threadpool_info
+        info = [x for x in threadpool_info() if x.get("user_api") == "blas"]
+        if info:
+            return int(info[0]["num_threads"])
+    except Exception:
+        pass
+    return len(os.sched_getaffinity(0))
+
+
+# ----------------------------------------------------------------------------- reference arm
+def run_reference(args, rank, world):
+    cfg = CONFIGS[args.config]
+    units = cfg["batch"] * cfg["heads"]
+    if rank != 0:
+        return 0
+    times = []
+    for i in range(args.warmup + args.steps):
+        t0 = time.perf_counter()
+        t_mask, t_head, n = oracle_sample(0, (i * 7) % units, budget_s=2.0, max_heads=1)
+        est_ms = (t_mask + units * t_head) * 1e3 / 2.0
+        if i >= args.warmup:
+            times.append(est_ms)
+    v = statistics.median(times)
+    line = {
+        "impl": "reference", "metric": METRIC, "value": round(v, 3), "unit": "ms/layer",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(2 * v, 3), "higher_is_better": False, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": cfg["name"], "units_bh": units, "target_scale": K_T,
+                   "decision_scale": S_D, "block": BLOCK, "head_dim": D, "layers_per_step": 2},
+        "cpu_baseline": {"value": round(v, 3), "unit": "ms/layer", "cores": cpu_cores(),
+                         "kind": "oracle",
+                         "sample": "per step: CSLA mask once + predictor/map/merge/2 attentions for "
+                                   "1 of %d (b,h) units, extrapolated to all units" % units},
+        "e2e": {"value": round(v, 3), "unit": "ms/layer", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ----------------------------------------------------------------------------- our arm
+def main():
+    args = parse()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        return run_reference(args, rank, world)
+
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    torch.cuda.set_device(local_rank)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    import paper_2602_04361_b200 as sv
+    from synth import kv_cache_iid, q_iid
+
+    cfg = CONFIGS[args.config]
+    units = cfg["batch"] * cfg["heads"]
+    bh0 = rank * units
+    n_q, n_qS = SIDES[K_T - 1] ** 2, SIDES[S_D - 1] ** 2
+    n_kv = sum(s * s for s in SIDES[:K_T])
+    dev = torch.device("cuda", local_rank)
+    q = q_iid(0, K_T, bh0, units, n_q, D, device=dev)
+    qS = q_iid(0, S_D, bh0, units, n_qS, D, device=dev)
+    k, v = kv_cache_iid(0, bh0, units, n_kv, D, device=dev)
+    layer = sv.SparseLayer(SIDES, K_T, S_D, BLOCK, units, sink_scales=SINK, windows=WINDOWS,
+                           topk=TOPK)
+    o_csla = torch.empty_like(q)
+    o_cs4a = torch.empty_like(q)
+    stream = torch.cuda.current_stream()
+    ev_attn = []     # (start, end) events around every CSLA attention launch in the timed region
+
+    def step(record=False):
+        layer.build_patterns(qS, k)
+        if record:
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+        layer.attend("csla", q, k, v, o=o_csla)
+        if record:
+            e1.record(stream)
+            ev_attn.append((e0, e1))
+        layer.attend("cs4a", q, k, v, o=o_cs4a)
+
+    LAUNCHES_PER_STEP = 8   # local_mask, predictor, map, 3x build_lists, 2x attention
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    assert layer.status.item() == 0, "device-side list status %d" % layer.status.item()
+
+    clocks = ClockSampler(local_rank)
+    clocks.start()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    t0 = torch.cuda.Event(enable_timing=True)
+    t1 = torch.cuda.Event(enable_timing=True)
+    t0.record(stream)
+    for _ in range(args.steps):
+        step(record=True)
+    t1.record(stream)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clk = clocks.stop()
+    ms_step = t0.elapsed_time(t1) / args.steps
+    attn_ms = statistics.mean(a.elapsed_time(b) for a, b in ev_attn)
+    if world > 1:
+        t = torch.tensor([ms_step, attn_ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms_step, attn_ms = float(t[0]), float(t[1])
+
+    # --- dense denominator (a7), same shape, separately timed
+    for _ in range(2):
+        sv.dense_attn(SIDES, K_T, q, k, v, o=o_cs4a)
+    torch.cuda.synchronize()
+    d0, d1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    nd = max(3, args.steps // 4)
+    d0.record(stream)
+    for _ in range(nd):
+        sv.dense_attn(SIDES, K_T, q, k, v, o=o_cs4a)
+    d1.record(stream)
+    torch.cuda.synchronize()
+    dense_ms = d0.elapsed_time(d1) / nd
+
+    # --- end to end through the public API with host buffers (pinned), copies timed
+    hq, hqS, hk, hv = (x.cpu().pin_memory() for x in (q, qS, k, v))
+    ho1, ho2 = torch.empty_like(hq).pin_memory(), torch.empty_like(hq).pin_memory()
+    ne = max(3, args.steps // 4)
+    for _ in range(2):
+        q.copy_(hq, non_blocking=True)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(ne):
+        q.copy_(hq, non_blocking=True)
+        qS.copy_(hqS, non_blocking=True)
+        k.copy_(hk, non_blocking=True)
+        v.copy_(hv, non_blocking=True)
+        step()
+        ho1.copy_(o_csla, non_blocking=True)
+        ho2.copy_(o_cs4a, non_blocking=True)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    e2e_step = e0.elapsed_time(e1) / ne
+    if world > 1:
+        t = torch.tensor([e2e_step], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_step = float(t[0])
+    h2d = sum(x.numel() * x.element_size() for x in (hq, hqS, hk, hv))
+    d2h = 2 * hq.numel() * hq.element_size()
+
+    # --- FLOP accounting for the CSLA kernel (lists copied once, outside timing)
+    rp, ci = layer.lists["csla"]
+    rp_h, ci_h = rp.cpu().numpy(), ci.cpu().numpy()
+    g_q = layer.gk["G_q"]
+    lists0 = [ci_h[rp_h[u]:rp_h[u + 1]] for u in range(g_q)]
+    alg_flops = algorithmic_flops(lists0, n_q, n_kv, BLOCK, D) * units   # mask shared by heads
+    nnz = int(rp_h[-1])
+    exec_flops = 4 * D * BLOCK * BLOCK * nnz
+    rp2 = layer.lists["cs4a"][0].cpu().numpy()
+    pk, src = peaks()
+    peak_tf = float(pk.get("bf16_tflops", 1590.0))
+    achieved_tf = alg_flops / (attn_ms * 1e-3) / 1e12
+    exec_tf = exec_flops / (attn_ms * 1e-3) / 1e12
+
+    # --- validation all-gather (untimed): each rank's sampled output rows -> rank 0 vs oracle
+    sample_rows = torch.tensor([0, 1, 2047, 4095], device=dev)
+    samp = o_csla[0].index_select(0, sample_rows).float().contiguous()
+    if world > 1:
+        gath = torch.empty((world,) + tuple(samp.shape), device=dev)
+        dist.all_gather_into_tensor(gath, samp)
+    else:
+        gath = samp.unsqueeze(0)
+    validation = None
+    if rank == 0:
+        from oracle.attention import block_sparse, merge_lists
+        from oracle.csla import local_block_mask
+        from oracle.geometry import Schedule
+        sched = Schedule(SIDES)
+        lists = merge_lists([local_block_mask(sched, K_T, BLOCK, SINK, WINDOWS)])
+        worst = 0.0
+        for r in range(world):
+            qq = q_iid(0, K_T, r * units, 1, n_q, D)[0].double().numpy()
+            kk, vv = kv_cache_iid(0, r * units, 1, n_kv, D)
+            rows_u = sorted({int(x) // BLOCK for x in sample_rows.tolist()})
+            want = block_sparse(qq, kk[0].double().numpy(), vv[0].double().numpy(), n_kv, BLOCK,
+                                lists, rows=rows_u)
+            got = gath[r].double().cpu().numpy()
+            worst = max(worst, float(np.abs(got - want[sample_rows.cpu().numpy()]).max()))
+        validation = {"sampled_rows_max_abs": worst, "ok": worst <= 1e-2,
+                      "collective": "all_gather_into_tensor" if world > 1 else "none"}
+
+    cpu_baseline = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        t_mask, t_head, n = oracle_sample(0, 0, budget_s=15.0, max_heads=8)
+        cpu_ms = (t_mask + units * t_head) * 1e3 / 2.0
+        cpu_baseline = {"value": round(cpu_ms, 2), "unit": "ms/layer", "cores": cpu_cores(),
+                        "kind": "oracle",
+                        "sample": f"CSLA mask once + predictor/map/merge/2 attentions for {n} of "
+                                  f"{units} (b,h) units, extrapolated to all units"}
+
+    if rank == 0:
+        value = ms_step / 2.0
+        line = {
+            "metric": METRIC, "value": round(value, 4), "unit": "ms/layer", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_step, 4),
+            "higher_is_better": False, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
+            "data": "synthetic (seeded counter-based iid N(0,1), bf16)",
+            "config": {"workload": cfg["name"], "units_bh_per_gpu": units, "batch_per_gpu": cfg["batch"],
+                       "heads": cfg["heads"], "target_scale": K_T, "q_len": n_q, "kv_len": n_kv,
+                       "decision_scale": S_D, "block": BLOCK, "head_dim": D, "sink_scales": SINK,
+                       "windows": list(WINDOWS), "topk": TOPK, "layers_per_step": 2,
+                       "parallelism": f"dp{world} over (batch x head)",
+                       "l2": "inputs > L2 (%.0f MB per GPU)" % ((q.numel() + qS.numel() + 2 * k.numel()) * 2 / 1e6)},
+            "roofline": {"bound": "tensor", "kernel": "attn_fwd_kernel<128,128> (CSLA lists)",
+                         "achieved": round(achieved_tf, 1), "peak": peak_tf, "unit": "TFLOP/s",
+                         "frac": round(achieved_tf / peak_tf, 4),
+                         "traffic": traffic_from_profile(),
+                         "peak_source": f"{src} bf16_tflops (burst)",
+                         "flops_per_launch": alg_flops, "launch_ms": round(attn_ms, 4)},
+            "tensor_util_executed": round(exec_tf / peak_tf, 4),
+            "csla_attn_ms": round(attn_ms, 4), "dense_attn_ms": round(dense_ms, 4),
+            "speedup_vs_dense": round(dense_ms / attn_ms, 3),
+            "csla_active_blocks_per_head": nnz // units,
+            "cs4a_active_blocks_per_head": int(rp2[-1]) // units,
+            "e2e": {"value": round(e2e_step / 2.0, 4), "unit": "ms/layer",
+                    "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
+            "gpu_launches": LAUNCHES_PER_STEP * args.steps,
+            "clocks": clk, "cpu_baseline": cpu_baseline, "validation": validation,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

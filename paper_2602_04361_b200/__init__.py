@@ -1,0 +1,273 @@
+"""Python binding of libsparvar.so — SparVAR's block-sparse cross-scale attention hot path on
+sm_100a (B200).  Argument marshalling only: every step of the path runs in the CUDA kernels of
+the C ABI declared in include/sparvar.h; PyTorch only provides device memory and streams.
+
+There is no CPU or PyTorch fallback.  If libsparvar.so is missing the import of this module
+raises (build it with `python -m paper_2602_04361_b200.build` or `__graft_entry__.build()`).
+
+Functions mirror the ABI names:
+    local_mask, predict_pattern, map_indices, build_block_lists, block_sparse_attn, dense_attn
+plus `geometry()` (block counts of a schedule) and `SparseLayer`, the user-facing composition of
+the whole path for one layer at the target scale.
+"""
+from __future__ import annotations
+
+import ctypes
+import math
+import os
+from typing import Optional, Sequence, Tuple
+
+import torch
+
+__all__ = [
+    "lib", "SparVARError", "geometry", "local_mask", "predict_pattern", "map_indices",
+    "build_block_lists", "block_sparse_attn", "dense_attn", "SparseLayer", "unpack_bits",
+    "SELECT_TOPK", "SELECT_THRESHOLD", "MAP_FOOTPRINT", "MAP_POINT",
+]
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libsparvar.so")
+
+SELECT_TOPK, SELECT_THRESHOLD = 0, 1
+MAP_FOOTPRINT, MAP_POINT = 0, 1
+_STATUS = {0: "OK", 1: "INVALID_ARG", 2: "SCHEDULE", 3: "UNSUPPORTED", 4: "CAPACITY",
+           5: "EMPTY_ROW", 6: "CUDA"}
+
+
+class SparVARError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"sparvar {_STATUS.get(status, status)}: {msg}")
+        self.status = status
+
+
+class _Schedule(ctypes.Structure):
+    _fields_ = [("num_scales", ctypes.c_int32), ("sides", ctypes.POINTER(ctypes.c_int32))]
+
+
+class _Shape(ctypes.Structure):
+    _fields_ = [("batch_heads", ctypes.c_int32), ("head_dim", ctypes.c_int32),
+                ("q_stride_bh", ctypes.c_int64), ("kv_stride_bh", ctypes.c_int64),
+                ("o_stride_bh", ctypes.c_int64)]
+
+
+def _load():
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"{LIB_PATH} not built: run `python -m paper_2602_04361_b200.build`")
+    L = ctypes.CDLL(LIB_PATH)
+    P, I32, I64, F32 = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64, ctypes.c_float
+    S = ctypes.POINTER(_Schedule)
+    SH = ctypes.POINTER(_Shape)
+    sig = {
+        "sparvar_local_mask": [S, I32, I32, I32, P, I32, P, P],
+        "sparvar_predict_pattern": [S, I32, I32, I32, SH, P, P, F32, I32, I32, F32, P, P, P],
+        "sparvar_map_indices": [S, I32, I32, I32, I32, I32, I32, P, P, P],
+        "sparvar_build_block_lists": [I32, I32, I32, P, P, I32, P, P, I64, P, P],
+        "sparvar_block_sparse_attn": [S, I32, I32, SH, P, P, P, P, P, F32, P, P, P],
+        "sparvar_dense_attn": [S, I32, SH, P, P, P, F32, P, P, P],
+    }
+    for name, args in sig.items():
+        f = getattr(L, name)
+        f.argtypes = args
+        f.restype = ctypes.c_int
+    L.sparvar_last_error.restype = ctypes.c_char_p
+    L.sparvar_version.restype = ctypes.c_int32
+    return L
+
+
+lib = _load()
+
+
+def _check(status: int):
+    if status != 0:
+        raise SparVARError(status, lib.sparvar_last_error().decode())
+
+
+def _sched(sides: Sequence[int]):
+    arr = (ctypes.c_int32 * len(sides))(*[int(s) for s in sides])
+    s = _Schedule(len(sides), arr)
+    s._keep = arr
+    return s
+
+
+def _stream(stream=None):
+    if stream is None:
+        stream = torch.cuda.current_stream()
+    return ctypes.c_void_p(stream.cuda_stream)
+
+
+def _ptr(t: Optional[torch.Tensor]):
+    return ctypes.c_void_p(0 if t is None else t.data_ptr())
+
+
+def _bh_view(t: torch.Tensor, name: str):
+    if t.dim() != 3 or t.dtype != torch.bfloat16 or not t.is_cuda:
+        raise ValueError(f"{name} must be a (BH, rows, D) bf16 CUDA tensor")
+    if t.stride(2) != 1 or t.stride(1) != t.shape[2]:
+        raise ValueError(f"{name}: rows must be contiguous (stride (.., D, 1))")
+    return t.stride(0)
+
+
+def geometry(sides: Sequence[int], scale: int, block: int) -> dict:
+    """Sizes of scale `scale` (1-based): N, C, G_q, G_kv and the bit-row width W."""
+    N = sides[scale - 1] ** 2
+    C = sum(s * s for s in sides[:scale])
+    g_q, g_kv = -(-N // block), -(-C // block)
+    return {"N": N, "C": C, "G_q": g_q, "G_kv": g_kv, "W": -(-g_kv // 32)}
+
+
+def unpack_bits(words: torch.Tensor, n: int) -> torch.Tensor:
+    """Bit rows (..., W) uint32/int32 -> bool (..., n), bit v%32 of word v/32."""
+    w = words.to(torch.int64) & 0xFFFFFFFF
+    bits = (w.unsqueeze(-1) >> torch.arange(32, device=w.device)) & 1
+    return bits.reshape(*w.shape[:-1], -1)[..., :n].bool()
+
+
+def local_mask(sides, target: int, block: int, sink_scales: int = 5,
+               windows: Sequence[int] = (7, 5, 3, 1, 1), out: Optional[torch.Tensor] = None,
+               stream=None) -> torch.Tensor:
+    g = geometry(sides, target, block)
+    if out is None:
+        out = torch.empty((g["G_q"], g["W"]), dtype=torch.int32, device="cuda")
+    w = (ctypes.c_int32 * max(1, len(windows)))(*[int(x) for x in windows])
+    _check(lib.sparvar_local_mask(ctypes.byref(_sched(sides)), target, block, sink_scales, w,
+                                  len(windows), _ptr(out), _stream(stream)))
+    return out
+
+
+def predict_pattern(sides, decision_scale: int, block: int, sink_scales: int, q_S: torch.Tensor,
+                    k_cache: torch.Tensor, mode: int = SELECT_TOPK, topk: int = 1,
+                    threshold: float = 0.0, softmax_scale: float = 0.0, want_mass: bool = True,
+                    mask_out=None, mass_out=None, stream=None):
+    g = geometry(sides, decision_scale, block)
+    bh, D = q_S.shape[0], q_S.shape[2]
+    sh = _Shape(bh, D, _bh_view(q_S, "q_S"), _bh_view(k_cache, "k_cache"), 0)
+    if mask_out is None:
+        mask_out = torch.empty((bh, g["G_q"], g["W"]), dtype=torch.int32, device="cuda")
+    if want_mass and mass_out is None:
+        mass_out = torch.empty((bh, g["G_q"], g["G_kv"]), dtype=torch.float32, device="cuda")
+    _check(lib.sparvar_predict_pattern(ctypes.byref(_sched(sides)), decision_scale, block,
+                                       sink_scales, ctypes.byref(sh), _ptr(q_S), _ptr(k_cache),
+                                       softmax_scale, mode, topk, threshold,
+                                       _ptr(mass_out if want_mass else None), _ptr(mask_out),
+                                       _stream(stream)))
+    return mask_out, (mass_out if want_mass else None)
+
+
+def map_indices(sides, src_scale: int, dst_scale: int, block: int, sink_scales: int,
+                src_mask: torch.Tensor, mode: int = MAP_FOOTPRINT, out=None, stream=None):
+    bh = src_mask.shape[0]
+    g = geometry(sides, dst_scale, block)
+    if out is None:
+        out = torch.empty((bh, g["G_q"], g["W"]), dtype=torch.int32, device="cuda")
+    _check(lib.sparvar_map_indices(ctypes.byref(_sched(sides)), src_scale, dst_scale, block,
+                                   sink_scales, mode, bh, _ptr(src_mask), _ptr(out),
+                                   _stream(stream)))
+    return out
+
+
+def build_block_lists(bh: int, g_q: int, g_kv: int, masks: Sequence[Tuple[torch.Tensor, bool]],
+                      capacity: Optional[int] = None, row_ptr=None, col_idx=None, status=None,
+                      stream=None):
+    """masks: [(bit-row tensor, broadcast)], broadcast masks are (g_q, W), others (bh, g_q, W).
+    Returns (row_ptr, col_idx, status) — status is a device int32 (0 = OK)."""
+    if capacity is None:
+        capacity = bh * g_q * g_kv
+    if row_ptr is None:
+        row_ptr = torch.empty(bh * g_q + 1, dtype=torch.int32, device="cuda")
+    if col_idx is None:
+        col_idx = torch.empty(max(1, capacity), dtype=torch.int32, device="cuda")
+    if status is None:
+        status = torch.zeros(1, dtype=torch.int32, device="cuda")
+    ptrs = (ctypes.c_void_p * len(masks))(*[m.data_ptr() for m, _ in masks])
+    bc = (ctypes.c_int32 * len(masks))(*[1 if b else 0 for _, b in masks])
+    _check(lib.sparvar_build_block_lists(bh, g_q, g_kv, ptrs, bc, len(masks), _ptr(row_ptr),
+                                         _ptr(col_idx), capacity, _ptr(status), _stream(stream)))
+    return row_ptr, col_idx, status
+
+
+def _attn_shape(q, k, o):
+    return _Shape(q.shape[0], q.shape[2], _bh_view(q, "q"), _bh_view(k, "k_cache"),
+                  _bh_view(o, "o"))
+
+
+def block_sparse_attn(sides, target: int, block: int, q: torch.Tensor, k_cache: torch.Tensor,
+                      v_cache: torch.Tensor, row_ptr: torch.Tensor, col_idx: torch.Tensor,
+                      softmax_scale: float = 0.0, o=None, lse=None, stream=None):
+    if o is None:
+        o = torch.empty_like(q)
+    if _bh_view(v_cache, "v_cache") != k_cache.stride(0):
+        raise ValueError("k_cache and v_cache must share a (b,h) stride")
+    sh = _attn_shape(q, k_cache, o)
+    _check(lib.sparvar_block_sparse_attn(ctypes.byref(_sched(sides)), target, block,
+                                         ctypes.byref(sh), _ptr(q), _ptr(k_cache), _ptr(v_cache),
+                                         _ptr(row_ptr), _ptr(col_idx), softmax_scale, _ptr(o),
+                                         _ptr(lse), _stream(stream)))
+    return o
+
+
+def dense_attn(sides, target: int, q, k_cache, v_cache, softmax_scale: float = 0.0, o=None,
+               lse=None, stream=None):
+    if o is None:
+        o = torch.empty_like(q)
+    if _bh_view(v_cache, "v_cache") != k_cache.stride(0):
+        raise ValueError("k_cache and v_cache must share a (b,h) stride")
+    sh = _attn_shape(q, k_cache, o)
+    _check(lib.sparvar_dense_attn(ctypes.byref(_sched(sides)), target, ctypes.byref(sh), _ptr(q),
+                                  _ptr(k_cache), _ptr(v_cache), softmax_scale, _ptr(o), _ptr(lse),
+                                  _stream(stream)))
+    return o
+
+
+class SparseLayer:
+    """The whole hot path for one attention layer at target scale K:
+
+        CSLA layer : local_mask(K) -> build_block_lists([local]) -> block_sparse_attn
+        CS4A layer : predict_pattern(S) -> map_indices(S->K) -> build_block_lists([mapped])
+                     -> block_sparse_attn
+        union      : all three masks OR-ed (READING 19)
+
+    Buffers for masks and lists are allocated once (sized from the geometry) and reused, so a
+    step is kernel launches only.
+    """
+
+    def __init__(self, sides, target: int, decision: int, block: int, bh: int,
+                 sink_scales: int = 5, windows=(7, 5, 3, 1, 1), select_mode=SELECT_TOPK,
+                 topk: int = 5, threshold: float = 0.01, map_mode=MAP_FOOTPRINT):
+        self.sides, self.K, self.S, self.B, self.bh = list(sides), target, decision, block, bh
+        self.sink, self.windows = sink_scales, tuple(windows)
+        self.select_mode, self.topk, self.threshold, self.map_mode = select_mode, topk, threshold, map_mode
+        gk, gs = geometry(sides, target, block), geometry(sides, decision, block)
+        self.gk, self.gs = gk, gs
+        dev = "cuda"
+        self.local = torch.empty((gk["G_q"], gk["W"]), dtype=torch.int32, device=dev)
+        self.src = torch.empty((bh, gs["G_q"], gs["W"]), dtype=torch.int32, device=dev)
+        self.mass = torch.empty((bh, gs["G_q"], gs["G_kv"]), dtype=torch.float32, device=dev)
+        self.mapped = torch.empty((bh, gk["G_q"], gk["W"]), dtype=torch.int32, device=dev)
+        cap = bh * gk["G_q"] * gk["G_kv"]
+        self.lists = {}
+        for name in ("csla", "cs4a", "union"):
+            self.lists[name] = (torch.empty(bh * gk["G_q"] + 1, dtype=torch.int32, device=dev),
+                                torch.empty(cap, dtype=torch.int32, device=dev))
+        self.status = torch.zeros(1, dtype=torch.int32, device=dev)
+        self.cap = cap
+
+    def build_patterns(self, q_S, k_cache, stream=None):
+        """a1-a5: CSLA mask, decision-scale prediction, mapping, and the three CSR list sets."""
+        local_mask(self.sides, self.K, self.B, self.sink, self.windows, out=self.local, stream=stream)
+        predict_pattern(self.sides, self.S, self.B, self.sink, q_S, k_cache, self.select_mode,
+                        self.topk, self.threshold, mask_out=self.src, mass_out=self.mass,
+                        stream=stream)
+        map_indices(self.sides, self.S, self.K, self.B, self.sink, self.src, self.map_mode,
+                    out=self.mapped, stream=stream)
+        g = self.gk
+        for name, masks in (("csla", [(self.local, True)]), ("cs4a", [(self.mapped, False)]),
+                            ("union", [(self.local, True), (self.mapped, False)])):
+            rp, ci = self.lists[name]
+            build_block_lists(self.bh, g["G_q"], g["G_kv"], masks, self.cap, rp, ci, self.status,
+                              stream=stream)
+
+    def attend(self, which: str, q, k_cache, v_cache, o=None, lse=None, stream=None):
+        """a6 on the lists `which` in {'csla', 'cs4a', 'union'}."""
+        rp, ci = self.lists[which]
+        return block_sparse_attn(self.sides, self.K, self.B, q, k_cache, v_cache, rp, ci, o=o,
+                                 lse=lse, stream=stream)

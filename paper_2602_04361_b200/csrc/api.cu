@@ -1,0 +1,324 @@
+// api.cu — the C ABI of libsparvar.so (include/sparvar.h): host-side validation, scale geometry,
+// TMA tensor-map construction and kernel launches.  No state is kept between calls.
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <string>
+
+#include "../../include/sparvar.h"
+#include "kernels.h"
+
+namespace {
+
+thread_local std::string g_err;
+
+sparvar_status fail(sparvar_status s, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return s;
+}
+
+sparvar_status cuda_fail(cudaError_t e, const char* what) {
+  return fail(SPARVAR_ERR_CUDA, "%s: %s", what, cudaGetErrorString(e));
+}
+
+sparvar_status ok() {
+  g_err.clear();
+  return SPARVAR_OK;
+}
+
+// Schedule -> Geo.  Sides non-decreasing, >= 1.
+sparvar_status make_geo(const sparvar_schedule* s, sv::Geo* g) {
+  if (s == nullptr || s->sides == nullptr) return fail(SPARVAR_ERR_INVALID_ARG, "null schedule");
+  if (s->num_scales < 1 || s->num_scales > sv::kMaxScales)
+    return fail(SPARVAR_ERR_SCHEDULE, "num_scales %d not in [1, %d]", s->num_scales, sv::kMaxScales);
+  *g = sv::Geo{};
+  g->K = s->num_scales;
+  long long c = 0;
+  g->cum[0] = 0;
+  for (int i = 0; i < s->num_scales; ++i) {
+    const int side = s->sides[i];
+    if (side < 1) return fail(SPARVAR_ERR_SCHEDULE, "side[%d] = %d < 1", i, side);
+    if (i > 0 && side < s->sides[i - 1])
+      return fail(SPARVAR_ERR_SCHEDULE, "sides must be non-decreasing (side[%d] = %d < %d)", i,
+                  side, s->sides[i - 1]);
+    if (side > 46340) return fail(SPARVAR_ERR_SCHEDULE, "side[%d] too large", i);
+    g->side[i] = side;
+    c += (long long)side * side;
+    if (c >= (1LL << 31)) return fail(SPARVAR_ERR_SCHEDULE, "schedule exceeds 2^31 tokens");
+    g->cum[i + 1] = (int)c;
+  }
+  return SPARVAR_OK;
+}
+
+int ceil_div(long long a, long long b) { return (int)((a + b - 1) / b); }
+
+bool attn_block_ok(int b) { return b == 16 || b == 32 || b == 64 || b == 128; }
+
+// ---------------------------------------------------------------------------- TMA descriptors
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                  const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                  const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                  CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn encode_fn() {
+  static EncodeTiledFn fn = nullptr;
+  if (fn == nullptr) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPointByVersion("cuTensorMapEncodeTiled", &p, 12000, cudaEnableDefault,
+                                         &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiledFn>(p);
+  }
+  return fn;
+}
+
+// bf16 tensor viewed as (D, rows, bh): box (64, box_rows, 1), 128-byte swizzle.  Rows >= `rows`
+// of a slab are out of bounds and read as zeros (never the next slab's data).
+sparvar_status make_tmap(CUtensorMap* m, const void* base, int D, long long rows, int bh,
+                         long long stride_bh_elems, int box_rows) {
+  EncodeTiledFn fn = encode_fn();
+  if (fn == nullptr) return fail(SPARVAR_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+  cuuint64_t dims[3] = {(cuuint64_t)D, (cuuint64_t)rows, (cuuint64_t)bh};
+  cuuint64_t strides[2] = {(cuuint64_t)D * 2, (cuuint64_t)stride_bh_elems * 2};
+  cuuint32_t box[3] = {64, (cuuint32_t)box_rows, 1};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(base), dims, strides,
+                  box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(SPARVAR_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
+  return SPARVAR_OK;
+}
+
+sparvar_status check_shape(const sparvar_attn_shape* sh, long long n_q, long long n_kv, bool need_o) {
+  if (sh == nullptr) return fail(SPARVAR_ERR_INVALID_ARG, "null shape");
+  if (sh->head_dim != 64 && sh->head_dim != 128)
+    return fail(SPARVAR_ERR_UNSUPPORTED, "head_dim %d not in {64, 128}", sh->head_dim);
+  if (sh->batch_heads < 1 || sh->batch_heads > 65535)
+    return fail(SPARVAR_ERR_INVALID_ARG, "batch_heads %d not in [1, 65535]", sh->batch_heads);
+  const long long D = sh->head_dim;
+  if (sh->q_stride_bh < n_q * D || sh->q_stride_bh % 8)
+    return fail(SPARVAR_ERR_INVALID_ARG, "q_stride_bh must be >= N*D and a multiple of 8");
+  if (sh->kv_stride_bh < n_kv * D || sh->kv_stride_bh % 8)
+    return fail(SPARVAR_ERR_INVALID_ARG, "kv_stride_bh must be >= C_k*D and a multiple of 8");
+  if (need_o && (sh->o_stride_bh < n_q * D || sh->o_stride_bh % 8))
+    return fail(SPARVAR_ERR_INVALID_ARG, "o_stride_bh must be >= N*D and a multiple of 8");
+  return SPARVAR_OK;
+}
+
+bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
+
+}  // namespace
+
+extern "C" {
+
+const char* sparvar_last_error(void) { return g_err.c_str(); }
+
+int32_t sparvar_version(void) { return 100; }
+
+sparvar_status sparvar_local_mask(const sparvar_schedule* sched, int32_t target_scale,
+                                  int32_t block, int32_t sink_scales, const int32_t* windows,
+                                  int32_t num_windows, uint32_t* mask_out, void* stream) {
+  sv::Geo g;
+  sparvar_status s = make_geo(sched, &g);
+  if (s != SPARVAR_OK) return s;
+  if (target_scale < 1 || target_scale > g.K)
+    return fail(SPARVAR_ERR_INVALID_ARG, "target_scale %d not in [1, %d]", target_scale, g.K);
+  if (block < 1) return fail(SPARVAR_ERR_INVALID_ARG, "block %d < 1", block);
+  if (sink_scales < 0 || sink_scales > target_scale)
+    return fail(SPARVAR_ERR_INVALID_ARG, "sink_scales %d not in [0, %d]", sink_scales, target_scale);
+  if (num_windows < 0 || num_windows > sv::kMaxScales || (num_windows > 0 && windows == nullptr))
+    return fail(SPARVAR_ERR_INVALID_ARG, "bad windows array");
+  if (mask_out == nullptr) return fail(SPARVAR_ERR_INVALID_ARG, "null mask_out");
+  int rel[sv::kMaxScales] = {0};
+  for (int i = 0; i < num_windows; ++i) {
+    if (windows[i] < 0 || (windows[i] > 0 && windows[i] % 2 == 0))
+      return fail(SPARVAR_ERR_INVALID_ARG, "window %d must be 0 or odd", windows[i]);
+    rel[i] = windows[i];
+  }
+  cudaError_t e = sv::launch_local_mask(g, target_scale, block, sink_scales, rel, mask_out,
+                                        (cudaStream_t)stream);
+  if (e == cudaErrorInvalidValue)
+    return fail(SPARVAR_ERR_UNSUPPORTED, "mask row too wide for shared memory");
+  if (e != cudaSuccess) return cuda_fail(e, "local_mask launch");
+  return ok();
+}
+
+sparvar_status sparvar_predict_pattern(const sparvar_schedule* sched, int32_t decision_scale,
+                                       int32_t block, int32_t sink_scales,
+                                       const sparvar_attn_shape* shape, const uint16_t* q_S,
+                                       const uint16_t* k_cache, float softmax_scale,
+                                       int32_t select_mode, int32_t topk, float threshold,
+                                       float* mass_out, uint32_t* mask_out, void* stream) {
+  sv::Geo g;
+  sparvar_status s = make_geo(sched, &g);
+  if (s != SPARVAR_OK) return s;
+  const int S = decision_scale;
+  if (S < 1 || S > g.K) return fail(SPARVAR_ERR_INVALID_ARG, "decision_scale %d not in [1, %d]", S, g.K);
+  if (!attn_block_ok(block))
+    return fail(SPARVAR_ERR_UNSUPPORTED, "block %d not in {16, 32, 64, 128}", block);
+  if (sink_scales < 0 || sink_scales > S)
+    return fail(SPARVAR_ERR_INVALID_ARG, "sink_scales %d not in [0, %d]", sink_scales, S);
+  const long long n_q = (long long)g.side[S - 1] * g.side[S - 1];
+  const long long n_kv = g.cum[S];
+  s = check_shape(shape, n_q, n_kv, false);
+  if (s != SPARVAR_OK) return s;
+  if (q_S == nullptr || k_cache == nullptr || mask_out == nullptr)
+    return fail(SPARVAR_ERR_INVALID_ARG, "null tensor pointer");
+  if (!aligned16(q_S) || !aligned16(k_cache))
+    return fail(SPARVAR_ERR_INVALID_ARG, "tensor pointers must be 16-byte aligned");
+  if (select_mode != SPARVAR_SELECT_TOPK && select_mode != SPARVAR_SELECT_THRESHOLD)
+    return fail(SPARVAR_ERR_INVALID_ARG, "select_mode %d", select_mode);
+  if (select_mode == SPARVAR_SELECT_TOPK && topk < 1)
+    return fail(SPARVAR_ERR_INVALID_ARG, "topk %d < 1", topk);
+  if (select_mode == SPARVAR_SELECT_THRESHOLD && !std::isfinite(threshold))
+    return fail(SPARVAR_ERR_INVALID_ARG, "threshold must be finite");
+  const int D = shape->head_dim;
+  sv::PredArgs a{};
+  a.n_q = (int)n_q;
+  a.n_kv = (int)n_kv;
+  a.g_q = ceil_div(n_q, block);
+  a.g_kv = ceil_div(n_kv, block);
+  a.bh = shape->batch_heads;
+  const float scale = softmax_scale > 0.f ? softmax_scale : 1.0f / std::sqrt((float)D);
+  a.scale_log2 = scale * 1.4426950408889634f;
+  a.mode = select_mode;
+  a.topk = topk;
+  a.tau = threshold;
+  a.n_sink_blocks = sink_scales > 0 ? ceil_div(g.cum[sink_scales], block) : 0;
+  a.mass = mass_out;
+  a.mask = mask_out;
+  if (sv::predictor_smem_bytes(D, block, a.g_kv) > 227 * 1024)
+    return fail(SPARVAR_ERR_UNSUPPORTED,
+                "predictor statistics for %d KV blocks do not fit in shared memory", a.g_kv);
+  CUtensorMap tq, tk;
+  if ((s = make_tmap(&tq, q_S, D, n_q, a.bh, shape->q_stride_bh, 128)) != SPARVAR_OK) return s;
+  if ((s = make_tmap(&tk, k_cache, D, n_kv, a.bh, shape->kv_stride_bh, block)) != SPARVAR_OK) return s;
+  cudaError_t e = sv::launch_predictor(D, block, tq, tk, a, (cudaStream_t)stream);
+  if (e != cudaSuccess) return cuda_fail(e, "predictor launch");
+  return ok();
+}
+
+sparvar_status sparvar_map_indices(const sparvar_schedule* sched, int32_t src_scale,
+                                   int32_t dst_scale, int32_t block, int32_t sink_scales,
+                                   int32_t map_mode, int32_t batch_heads,
+                                   const uint32_t* src_mask, uint32_t* dst_mask, void* stream) {
+  sv::Geo g;
+  sparvar_status s = make_geo(sched, &g);
+  if (s != SPARVAR_OK) return s;
+  if (src_scale < 1 || dst_scale > g.K || src_scale > dst_scale)
+    return fail(SPARVAR_ERR_INVALID_ARG, "need 1 <= src_scale (%d) <= dst_scale (%d) <= %d",
+                src_scale, dst_scale, g.K);
+  if (block < 1) return fail(SPARVAR_ERR_INVALID_ARG, "block %d < 1", block);
+  if (sink_scales < 0 || sink_scales > dst_scale)
+    return fail(SPARVAR_ERR_INVALID_ARG, "sink_scales %d not in [0, %d]", sink_scales, dst_scale);
+  if (map_mode != SPARVAR_MAP_FOOTPRINT && map_mode != SPARVAR_MAP_POINT)
+    return fail(SPARVAR_ERR_INVALID_ARG, "map_mode %d", map_mode);
+  if (batch_heads < 1 || batch_heads > 65535)
+    return fail(SPARVAR_ERR_INVALID_ARG, "batch_heads %d", batch_heads);
+  if (src_mask == nullptr || dst_mask == nullptr)
+    return fail(SPARVAR_ERR_INVALID_ARG, "null mask pointer");
+  cudaError_t e = sv::launch_map_indices(g, src_scale, dst_scale, block, sink_scales, map_mode,
+                                         batch_heads, src_mask, dst_mask, (cudaStream_t)stream);
+  if (e == cudaErrorInvalidValue)
+    return fail(SPARVAR_ERR_UNSUPPORTED, "mask row too wide for shared memory");
+  if (e != cudaSuccess) return cuda_fail(e, "map launch");
+  return ok();
+}
+
+sparvar_status sparvar_build_block_lists(int32_t batch_heads, int32_t g_q, int32_t g_kv,
+                                         const uint32_t* const* masks, const int32_t* broadcast,
+                                         int32_t num_masks, int32_t* row_ptr, int32_t* col_idx,
+                                         int64_t col_capacity, int32_t* status_dev, void* stream) {
+  if (batch_heads < 1 || g_q < 1 || g_kv < 1)
+    return fail(SPARVAR_ERR_INVALID_ARG, "batch_heads, g_q, g_kv must be >= 1");
+  if ((long long)batch_heads * g_q >= (1LL << 31))
+    return fail(SPARVAR_ERR_INVALID_ARG, "too many rows");
+  if (num_masks < 1 || num_masks > 8 || masks == nullptr || broadcast == nullptr)
+    return fail(SPARVAR_ERR_INVALID_ARG, "need 1..8 masks");
+  if (row_ptr == nullptr || (col_idx == nullptr && col_capacity > 0) || col_capacity < 0)
+    return fail(SPARVAR_ERR_INVALID_ARG, "null row_ptr / col_idx");
+  sv::MaskSet ms{};
+  ms.n = num_masks;
+  for (int i = 0; i < num_masks; ++i) {
+    if (masks[i] == nullptr) return fail(SPARVAR_ERR_INVALID_ARG, "masks[%d] is null", i);
+    ms.ptr[i] = masks[i];
+    ms.broadcast[i] = broadcast[i] ? 1 : 0;
+  }
+  cudaError_t e = sv::launch_build_lists(batch_heads, g_q, g_kv, ms, row_ptr, col_idx,
+                                         col_capacity, status_dev, (cudaStream_t)stream);
+  if (e != cudaSuccess) return cuda_fail(e, "build_lists launch");
+  return ok();
+}
+
+static sparvar_status attn_common(const sparvar_schedule* sched, int32_t target_scale,
+                                  int32_t block, const sparvar_attn_shape* shape,
+                                  const uint16_t* q, const uint16_t* k, const uint16_t* v,
+                                  const int32_t* row_ptr, const int32_t* col_idx, float scale_in,
+                                  uint16_t* o, float* lse, void* stream) {
+  sv::Geo g;
+  sparvar_status s = make_geo(sched, &g);
+  if (s != SPARVAR_OK) return s;
+  if (target_scale < 1 || target_scale > g.K)
+    return fail(SPARVAR_ERR_INVALID_ARG, "target_scale %d not in [1, %d]", target_scale, g.K);
+  if (!attn_block_ok(block))
+    return fail(SPARVAR_ERR_UNSUPPORTED, "block %d not in {16, 32, 64, 128}", block);
+  const long long n_q = (long long)g.side[target_scale - 1] * g.side[target_scale - 1];
+  const long long n_kv = g.cum[target_scale];
+  s = check_shape(shape, n_q, n_kv, true);
+  if (s != SPARVAR_OK) return s;
+  if (q == nullptr || k == nullptr || v == nullptr || o == nullptr)
+    return fail(SPARVAR_ERR_INVALID_ARG, "null tensor pointer");
+  if (!aligned16(q) || !aligned16(k) || !aligned16(v) || !aligned16(o))
+    return fail(SPARVAR_ERR_INVALID_ARG, "tensor pointers must be 16-byte aligned");
+  const int D = shape->head_dim;
+  sv::AttnArgs a{};
+  a.n_q = (int)n_q;
+  a.n_kv = (int)n_kv;
+  a.g_q = ceil_div(n_q, block);
+  a.bh = shape->batch_heads;
+  a.row_ptr = row_ptr;
+  a.col_idx = col_idx;
+  const float scale = scale_in > 0.f ? scale_in : 1.0f / std::sqrt((float)D);
+  a.scale_log2 = scale * 1.4426950408889634f;
+  a.o = o;
+  a.o_stride = shape->o_stride_bh;
+  a.lse = lse;
+  CUtensorMap tq, tk, tv;
+  if ((s = make_tmap(&tq, q, D, n_q, a.bh, shape->q_stride_bh, 128)) != SPARVAR_OK) return s;
+  if ((s = make_tmap(&tk, k, D, n_kv, a.bh, shape->kv_stride_bh, block)) != SPARVAR_OK) return s;
+  if ((s = make_tmap(&tv, v, D, n_kv, a.bh, shape->kv_stride_bh, block)) != SPARVAR_OK) return s;
+  cudaError_t e = sv::launch_attention(D, block, tq, tk, tv, a, (cudaStream_t)stream);
+  if (e != cudaSuccess) return cuda_fail(e, "attention launch");
+  return ok();
+}
+
+sparvar_status sparvar_block_sparse_attn(const sparvar_schedule* sched, int32_t target_scale,
+                                         int32_t block, const sparvar_attn_shape* shape,
+                                         const uint16_t* q, const uint16_t* k_cache,
+                                         const uint16_t* v_cache, const int32_t* row_ptr,
+                                         const int32_t* col_idx, float softmax_scale,
+                                         uint16_t* o, float* lse, void* stream) {
+  if (row_ptr == nullptr || col_idx == nullptr)
+    return fail(SPARVAR_ERR_INVALID_ARG, "null row_ptr / col_idx");
+  return attn_common(sched, target_scale, block, shape, q, k_cache, v_cache, row_ptr, col_idx,
+                     softmax_scale, o, lse, stream);
+}
+
+sparvar_status sparvar_dense_attn(const sparvar_schedule* sched, int32_t target_scale,
+                                  const sparvar_attn_shape* shape, const uint16_t* q,
+                                  const uint16_t* k_cache, const uint16_t* v_cache,
+                                  float softmax_scale, uint16_t* o, float* lse, void* stream) {
+  return attn_common(sched, target_scale, 128, shape, q, k_cache, v_cache, nullptr, nullptr,
+                     softmax_scale, o, lse, stream);
+}
+
+}  // extern "C"

@@ -1,0 +1,69 @@
+// kernels.h — internal launch interface between api.cu (C ABI, validation, TMA descriptors) and
+// the kernel translation units.  Not part of the public ABI (see include/sparvar.h).
+#pragma once
+#include <cstdint>
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+namespace sv {
+
+constexpr int kMaxScales = 32;
+
+// Scale geometry copied by value into kernels (a few hundred bytes of kernel parameters).
+struct Geo {
+  int K;                          // number of scales in the schedule
+  int side[kMaxScales];           // s_1..s_K at [0..K)
+  int cum[kMaxScales + 1];        // C_0..C_K at [0..K]
+};
+
+// ------------------------------------------------------------------ masks.cu
+cudaError_t launch_local_mask(const Geo& g, int target, int block, int sink_scales,
+                              const int* windows_rel /*[kMaxScales], index = target - h*/,
+                              uint32_t* out, cudaStream_t st);
+cudaError_t launch_map_indices(const Geo& g, int S, int K, int block, int sink_scales, int mode,
+                               int bh, const uint32_t* src, uint32_t* dst, cudaStream_t st);
+struct MaskSet {
+  const uint32_t* ptr[8];
+  int broadcast[8];
+  int n;
+};
+cudaError_t launch_build_lists(int bh, int g_q, int g_kv, const MaskSet& ms, int* row_ptr,
+                               int* col_idx, long long cap, int* status, cudaStream_t st);
+
+// ------------------------------------------------------------------ attention.cu
+struct AttnArgs {
+  int n_q;            // N_K query rows per (b,h)
+  int n_kv;           // C_K valid cache rows
+  int g_q;            // ceil(N_K / block): CSR rows per (b,h)
+  int bh;             // batch*heads
+  const int* row_ptr; // nullptr -> dense (every block)
+  const int* col_idx;
+  float scale_log2;   // softmax_scale * log2(e)
+  uint16_t* o;
+  long long o_stride; // elements between (b,h) slabs of O
+  float* lse;
+};
+cudaError_t launch_attention(int head_dim, int block, const CUtensorMap& tq, const CUtensorMap& tk,
+                             const CUtensorMap& tv, const AttnArgs& a, cudaStream_t st);
+
+// ------------------------------------------------------------------ predictor.cu
+struct PredArgs {
+  int n_q;            // N_S
+  int n_kv;           // C_S
+  int g_q;            // ceil(N_S / block)
+  int g_kv;           // ceil(C_S / block)
+  int bh;
+  float scale_log2;
+  int mode;           // 0 top-k, 1 threshold
+  int topk;
+  float tau;
+  int n_sink_blocks;  // ceil(C_sink / block)
+  float* mass;        // nullable [bh][g_q][g_kv]
+  uint32_t* mask;     // [bh][g_q][W]
+};
+// Returns cudaErrorInvalidValue if the statistics do not fit (caller maps it to UNSUPPORTED).
+cudaError_t launch_predictor(int head_dim, int block, const CUtensorMap& tq, const CUtensorMap& tk,
+                             const PredArgs& a, cudaStream_t st);
+size_t predictor_smem_bytes(int head_dim, int block, int g_kv);
+
+}  // namespace sv

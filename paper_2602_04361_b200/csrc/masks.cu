@@ -1,0 +1,270 @@
+// masks.cu — integer kernels of the hot path: CSLA local block mask (a1), cross-scale index
+// mapping (a4), and merge + compaction of bit-row masks into CSR block lists (a5).
+//
+// All three are exact integer computations and are parity-tested bit for bit against the fp64 /
+// integer oracle (oracle/csla.py, oracle/mapping.py, oracle/attention.py), which follows the
+// paper token by token; these kernels instead mark contiguous flat-index ranges (a clipped window
+// row or a footprint row is one contiguous run of a scale's row-major layout) and so touch every
+// block a token run covers without visiting tokens one by one.
+#include <cstdio>
+
+#include "kernels.h"
+
+namespace sv {
+namespace {
+
+// round-half-to-even of p/q, q > 0, p of any sign (READING 3 / READING 15)
+__device__ __forceinline__ int rne_div(long long p, long long q) {
+  long long fl = p / q;
+  if ((p % q != 0) && ((p < 0) != (q < 0))) --fl;     // floor division
+  const long long rem2 = 2 * (p - fl * q);            // in [0, 2q)
+  if (rem2 > q || (rem2 == q && (fl & 1))) ++fl;
+  return static_cast<int>(fl);
+}
+
+// Set bits [b0, b1] of a shared bit row.
+__device__ __forceinline__ void set_bit_range(uint32_t* row, int b0, int b1) {
+  for (int w = b0 >> 5; w <= (b1 >> 5); ++w) {
+    const int lo = max(b0, w * 32) - w * 32;
+    const int hi = min(b1, w * 32 + 31) - w * 32;
+    const uint32_t m = (hi == 31 ? 0xffffffffu : ((1u << (hi + 1)) - 1u)) & ~((1u << lo) - 1u);
+    atomicOr(row + w, m);
+  }
+}
+
+// Flat token range [t0, t1] of the cache -> blocks.
+__device__ __forceinline__ void set_token_range(uint32_t* row, int t0, int t1, int B) {
+  set_bit_range(row, t0 / B, t1 / B);
+}
+
+// ------------------------------------------------------------------------------------ a1
+// One CTA per query block u.  Each thread takes query tokens of u; for every scale h with a
+// window it clips the Chebyshev square around the aligned coordinate and marks
+// the blocks each square row covers.  The sink prefix [0, C_sink) is a single range.
+struct WinArr {
+  int w[kMaxScales];   // w[i] = window of scale K - i
+};
+
+__global__ void local_mask_kernel(const Geo g, int K, int B, int sink_scales, const WinArr win,
+                                  int W, uint32_t* __restrict__ out) {
+  extern __shared__ uint32_t srow[];
+  const int u = blockIdx.x;
+  for (int w = threadIdx.x; w < W; w += blockDim.x) srow[w] = 0;
+  __syncthreads();
+  const int sK = g.side[K - 1];
+  const int nq = sK * sK;
+  if (threadIdx.x == 0 && sink_scales > 0) set_token_range(srow, 0, g.cum[sink_scales] - 1, B);
+  for (int t = u * B + threadIdx.x; t < min((u + 1) * B, nq); t += blockDim.x) {
+    const int x = t / sK, y = t % sK;
+    for (int h = 1; h <= K; ++h) {
+      const int w = win.w[K - h];
+      if (w <= 0) continue;
+      const int r = w / 2;
+      const int sh = g.side[h - 1];
+      const int xt = min(rne_div((long long)x * sh, sK), sh - 1);
+      const int yt = min(rne_div((long long)y * sh, sK), sh - 1);
+      const int x0 = max(0, xt - r), x1 = min(sh - 1, xt + r);
+      const int y0 = max(0, yt - r), y1 = min(sh - 1, yt + r);
+      const int base = g.cum[h - 1];
+      for (int xr = x0; xr <= x1; ++xr)
+        set_token_range(srow, base + xr * sh + y0, base + xr * sh + y1, B);
+    }
+  }
+  __syncthreads();
+  for (int w = threadIdx.x; w < W; w += blockDim.x) out[(long long)u * W + w] = srow[w];
+}
+
+// ------------------------------------------------------------------------------------ a4
+// One CTA per (target query block gq, bh).  Source row phi(gq); every real token of
+// every active source block is decomposed, aligned to l' = l + (K - S)
+// and projected (READING 14).
+__global__ void map_kernel(const Geo g, int S, int K, int B, int sink_scales, int mode, int G_S,
+                           int G_K, int W_S, int W_K, const uint32_t* __restrict__ src,
+                           uint32_t* __restrict__ dst) {
+  extern __shared__ uint32_t srow[];
+  const int gq = blockIdx.x;
+  const int bh = blockIdx.y;
+  for (int w = threadIdx.x; w < W_K; w += blockDim.x) srow[w] = 0;
+  __syncthreads();
+  int gs = rne_div(2LL * gq * G_S + G_S - G_K, 2LL * G_K);
+  gs = min(max(gs, 0), G_S - 1);
+  const uint32_t* srcrow = src + ((long long)bh * G_S + gs) * W_S;
+  const int n_kvS = g.cum[S];
+  const int shift = K - S;
+  for (int w = 0; w < W_S; ++w) {
+    uint32_t bits = __ldg(srcrow + w);
+    while (bits) {
+      const int v = w * 32 + __ffs(bits) - 1;
+      bits &= bits - 1;
+      for (int j = v * B + threadIdx.x; j < min((v + 1) * B, n_kvS); j += blockDim.x) {
+        int l = 1;
+        while (g.cum[l] <= j) ++l;                        // C_{l-1} <= j < C_l
+        const int delta = j - g.cum[l - 1];
+        const int lp = l + shift;
+        const int s = g.side[l - 1], sp = g.side[lp - 1];
+        const int x = delta / s, y = delta % s;
+        const int base = g.cum[lp - 1];
+        if (mode == 1) {                                   // POINT
+          const int xp = x * sp / s, yp = y * sp / s;
+          set_token_range(srow, base + xp * sp + yp, base + xp * sp + yp, B);
+        } else {                                           // FOOTPRINT (READING 14)
+          const int x0 = x * sp / s, x1 = (x + 1) * sp / s - 1;
+          const int y0 = y * sp / s, y1 = (y + 1) * sp / s - 1;
+          for (int xp = x0; xp <= x1; ++xp)
+            set_token_range(srow, base + xp * sp + y0, base + xp * sp + y1, B);
+        }
+      }
+    }
+  }
+  if (threadIdx.x == 0 && sink_scales > 0) set_token_range(srow, 0, g.cum[sink_scales] - 1, B);
+  __syncthreads();
+  uint32_t* drow = dst + ((long long)bh * G_K + gq) * W_K;
+  for (int w = threadIdx.x; w < W_K; w += blockDim.x) drow[w] = srow[w];
+}
+
+// ------------------------------------------------------------------------------------ a5
+// Single CTA of 1024 threads.  Phase 1: popcount of every OR-ed row -> row_ptr[r+1].  Phase 2:
+// block-wide exclusive scan over rows.  Phase 3: each warp compacts its rows: lane = word, warp
+// exclusive scan of popcounts (shuffle) gives each word's output offset, bits are emitted in
+// ascending order.
+__device__ __forceinline__ uint32_t row_word(const MaskSet& ms, int r, int u, int w, int W) {
+  uint32_t x = 0;
+  for (int i = 0; i < ms.n; ++i)
+    x |= __ldg(ms.ptr[i] + (long long)(ms.broadcast[i] ? u : r) * W + w);
+  return x;
+}
+
+__global__ void __launch_bounds__(1024) build_lists_kernel(int rows, int g_q, int g_kv, MaskSet ms,
+                                                           int* __restrict__ row_ptr,
+                                                           int* __restrict__ col_idx,
+                                                           long long cap, int* status) {
+  __shared__ int s_warp[32];
+  __shared__ int s_carry;
+  __shared__ int s_err;
+  const int W = (g_kv + 31) / 32;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  if (threadIdx.x == 0) {
+    s_carry = 0;
+    s_err = 0;
+  }
+  // phase 1
+  for (int r = warp; r < rows; r += nw) {
+    const int u = r % g_q;
+    int c = 0;
+    for (int w = lane; w < W; w += 32) c += __popc(row_word(ms, r, u, w, W));
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+    if (lane == 0) row_ptr[r + 1] = c;
+  }
+  __syncthreads();
+  // phase 2 (threads own consecutive rows of a 1024-row chunk)
+  for (int base = 0; base < rows; base += blockDim.x) {
+    const int r = base + threadIdx.x;
+    const int c = r < rows ? row_ptr[r + 1] : 0;
+    if (r < rows && c == 0) s_err = 5;
+    int inc = c;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int t = __shfl_up_sync(0xffffffffu, inc, o);
+      if (lane >= o) inc += t;
+    }
+    if (lane == 31) s_warp[warp] = inc;
+    __syncthreads();
+    if (warp == 0) {
+      int wv = lane < nw ? s_warp[lane] : 0;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int t = __shfl_up_sync(0xffffffffu, wv, o);
+        if (lane >= o) wv += t;
+      }
+      s_warp[lane] = wv;
+    }
+    __syncthreads();
+    const int carry = s_carry;
+    const int pre = (warp > 0 ? s_warp[warp - 1] : 0) + carry;
+    if (r < rows) row_ptr[r + 1] = pre + inc;
+    __syncthreads();
+    if (threadIdx.x == blockDim.x - 1) s_carry = pre + inc;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) row_ptr[0] = 0;
+  const long long nnz = s_carry;
+  if (nnz > cap) {
+    if (threadIdx.x == 0 && status) atomicCAS(status, 0, 4);
+    return;
+  }
+  if (threadIdx.x == 0 && status && s_err) atomicCAS(status, 0, s_err);
+  __syncthreads();
+  // phase 3
+  for (int r = warp; r < rows; r += nw) {
+    const int u = r % g_q;
+    int off = row_ptr[r];
+    for (int w0 = 0; w0 < W; w0 += 32) {
+      const int w = w0 + lane;
+      uint32_t x = w < W ? row_word(ms, r, u, w, W) : 0u;
+      const int c = __popc(x);
+      int inc = c;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int t = __shfl_up_sync(0xffffffffu, inc, o);
+        if (lane >= o) inc += t;
+      }
+      int pos = off + inc - c;
+      while (x) {
+        col_idx[pos++] = w * 32 + __ffs(x) - 1;
+        x &= x - 1;
+      }
+      off += __shfl_sync(0xffffffffu, inc, 31);
+    }
+  }
+}
+
+}  // namespace
+
+cudaError_t launch_local_mask(const Geo& g, int target, int block, int sink_scales,
+                              const int* windows_rel, uint32_t* out, cudaStream_t st) {
+  WinArr win;
+  for (int i = 0; i < kMaxScales; ++i) win.w[i] = windows_rel[i];
+  const int nq = g.side[target - 1] * g.side[target - 1];
+  const int gq = (nq + block - 1) / block;
+  const int gkv = (g.cum[target] + block - 1) / block;
+  const int W = (gkv + 31) / 32;
+  const size_t smem = size_t(W) * 4;
+  if (smem > 200 * 1024) return cudaErrorInvalidValue;
+  if (smem > 48 * 1024) {
+    cudaError_t e = cudaFuncSetAttribute(local_mask_kernel,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+  }
+  const int threads = block >= 256 ? 256 : (block >= 64 ? block : 64);
+  local_mask_kernel<<<gq, threads, smem, st>>>(g, target, block, sink_scales, win, W, out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_map_indices(const Geo& g, int S, int K, int block, int sink_scales, int mode,
+                               int bh, const uint32_t* src, uint32_t* dst, cudaStream_t st) {
+  const int nS = g.side[S - 1] * g.side[S - 1], nK = g.side[K - 1] * g.side[K - 1];
+  const int G_S = (nS + block - 1) / block, G_K = (nK + block - 1) / block;
+  const int W_S = ((g.cum[S] + block - 1) / block + 31) / 32;
+  const int W_K = ((g.cum[K] + block - 1) / block + 31) / 32;
+  const size_t smem = size_t(W_K) * 4;
+  if (smem > 200 * 1024) return cudaErrorInvalidValue;
+  if (smem > 48 * 1024) {
+    cudaError_t e = cudaFuncSetAttribute(map_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)smem);
+    if (e != cudaSuccess) return e;
+  }
+  dim3 grid(G_K, bh);
+  const int threads = block >= 128 ? 128 : 64;
+  map_kernel<<<grid, threads, smem, st>>>(g, S, K, block, sink_scales, mode, G_S, G_K, W_S, W_K,
+                                          src, dst);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_build_lists(int bh, int g_q, int g_kv, const MaskSet& ms, int* row_ptr,
+                               int* col_idx, long long cap, int* status, cudaStream_t st) {
+  build_lists_kernel<<<1, 1024, 0, st>>>(bh * g_q, g_q, g_kv, ms, row_ptr, col_idx, cap, status);
+  return cudaGetLastError();
+}
+
+}  // namespace sv

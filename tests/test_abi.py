@@ -1,0 +1,107 @@
+"""CPU-only checks of the C ABI library: it loads, exports every symbol include/sparvar.h
+declares, and rejects bad arguments on the host (no kernel is launched on these paths)."""
+import ctypes
+import os
+import re
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HEADER = os.path.join(ROOT, "include", "sparvar.h")
+
+
+@pytest.fixture(scope="module")
+def sv():
+    from paper_2602_04361_b200 import build as b
+    b.build()
+    import paper_2602_04361_b200 as pkg
+    return pkg
+
+
+def _declared():
+    txt = open(HEADER).read()
+    return sorted(set(re.findall(r"\b(sparvar_[a-z_]+)\s*\(", txt)))
+
+
+def test_exports_every_declared_symbol(sv):
+    names = _declared()
+    assert "sparvar_block_sparse_attn" in names and len(names) == 8
+    L = ctypes.CDLL(sv.LIB_PATH)
+    for n in names:
+        assert hasattr(L, n), n
+
+
+def test_version_and_error_string(sv):
+    assert sv.lib.sparvar_version() == 100
+    assert isinstance(sv.lib.sparvar_last_error(), bytes)
+
+
+def _sched(sv, sides):
+    return ctypes.byref(sv._sched(sides))
+
+
+def test_schedule_validation(sv):
+    out = ctypes.c_void_p(16)   # never dereferenced: validation fails first
+    w = (ctypes.c_int32 * 1)(3)
+    st = sv.lib.sparvar_local_mask(_sched(sv, [2, 1]), 2, 16, 0, w, 1, out, None)
+    assert st == 2 and b"non-decreasing" in sv.lib.sparvar_last_error()
+    st = sv.lib.sparvar_local_mask(_sched(sv, [1, 2]), 3, 16, 0, w, 1, out, None)
+    assert st == 1
+    w2 = (ctypes.c_int32 * 1)(4)
+    st = sv.lib.sparvar_local_mask(_sched(sv, [1, 2]), 2, 16, 0, w2, 1, out, None)
+    assert st == 1 and b"odd" in sv.lib.sparvar_last_error()
+
+
+def test_attention_validation(sv):
+    sh = sv._Shape(1, 96, 64 * 96, 85 * 96, 64 * 96)     # head_dim 96 unsupported
+    p = ctypes.c_void_p(256)
+    st = sv.lib.sparvar_dense_attn(_sched(sv, [1, 2, 4, 8]), 4, ctypes.byref(sh), p, p, p, 0.0,
+                                   p, None, None)
+    assert st == 3
+    sh = sv._Shape(1, 64, 64 * 64, 80 * 64, 64 * 64)     # kv stride < C_K * D
+    st = sv.lib.sparvar_block_sparse_attn(_sched(sv, [1, 2, 4, 8]), 4, 16, ctypes.byref(sh), p, p,
+                                          p, p, p, 0.0, p, None, None)
+    assert st == 1 and b"kv_stride" in sv.lib.sparvar_last_error()
+    sh = sv._Shape(1, 64, 64 * 64, 85 * 64 + 3, 64 * 64)  # stride not a multiple of 8
+    st = sv.lib.sparvar_dense_attn(_sched(sv, [1, 2, 4, 8]), 4, ctypes.byref(sh), p, p, p, 0.0,
+                                   p, None, None)
+    assert st == 1
+    sh = sv._Shape(1, 64, 64 * 64, 88 * 64, 64 * 64)
+    st = sv.lib.sparvar_block_sparse_attn(_sched(sv, [1, 2, 4, 8]), 4, 48, ctypes.byref(sh), p, p,
+                                          p, p, p, 0.0, p, None, None)
+    assert st == 3                                         # block 48 unsupported
+
+
+def test_predict_and_map_validation(sv):
+    p = ctypes.c_void_p(256)
+    sh = sv._Shape(1, 64, 16 * 64, 21 * 64, 0)
+    st = sv.lib.sparvar_predict_pattern(_sched(sv, [1, 2, 4, 8]), 3, 16, 0, ctypes.byref(sh), p, p,
+                                        0.0, 0, 0, 0.0, None, p, None)
+    assert st == 1 and b"topk" in sv.lib.sparvar_last_error()
+    st = sv.lib.sparvar_map_indices(_sched(sv, [1, 2, 4, 8]), 4, 3, 16, 0, 0, 1, p, p, None)
+    assert st == 1
+    st = sv.lib.sparvar_map_indices(_sched(sv, [1, 2, 4, 8]), 3, 4, 16, 0, 7, 1, p, p, None)
+    assert st == 1
+
+
+def test_build_lists_validation(sv):
+    p = ctypes.c_void_p(256)
+    masks = (ctypes.c_void_p * 1)(256)
+    bc = (ctypes.c_int32 * 1)(0)
+    st = sv.lib.sparvar_build_block_lists(1, 1, 1, masks, bc, 0, p, p, 10, None, None)
+    assert st == 1
+    st = sv.lib.sparvar_build_block_lists(0, 1, 1, masks, bc, 1, p, p, 10, None, None)
+    assert st == 1
+
+
+def test_no_fallback_when_library_missing(tmp_path, monkeypatch):
+    """The binding raises on import when libsparvar.so is absent (no CPU fallback)."""
+    import importlib.util
+    import shutil
+    pkg = tmp_path / "paper_2602_04361_b200"
+    pkg.mkdir()
+    shutil.copy(os.path.join(ROOT, "paper_2602_04361_b200", "__init__.py"), pkg / "__init__.py")
+    spec = importlib.util.spec_from_file_location("sv_nolib", pkg / "__init__.py")
+    mod = importlib.util.module_from_spec(spec)
+    with pytest.raises(ImportError):
+        spec.loader.exec_module(mod)

@@ -1,0 +1,170 @@
+"""GPU parity of the block-sparse / dense attention kernel (a6/a7) through the C ABI against the
+fp64 oracle on the same bf16 inputs: max |diff| <= 1e-2 and mean |diff| <= 1e-3 (north_star)."""
+import numpy as np
+import pytest
+import torch
+
+from oracle.attention import block_sparse, dense, merge_lists
+from oracle.csla import local_block_mask
+from oracle.geometry import INFINITY_1K_SIDES, Schedule, ceil_div
+from synth import kv_cache_iid, q_iid
+from tests.helpers import (EQ256, INF2B, MAX_ABS, MEAN_ABS, TINY, attn_errors, bool_to_bits,
+                           csr_lists, to_np)
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def sv():
+    import paper_2602_04361_b200 as m
+    return m
+
+
+def _inputs(sides, K, D, bh, seed=0, cap_extra=0):
+    sched = Schedule(sides)
+    q = q_iid(seed, K, 0, bh, sched.N(K), D)
+    k, v = kv_cache_iid(seed, 0, bh, sched.C(K), D, capacity=sched.C(K) + cap_extra)
+    return sched, q.cuda(), k.cuda(), v.cuda()
+
+
+def _lists_from_bool(sv, masks_bh):
+    bh, gq, gkv = masks_bh.shape
+    return sv.build_block_lists(bh, gq, gkv, [(torch.from_numpy(bool_to_bits(masks_bh)).cuda(), False)])
+
+
+def _check(got, want, rows=None):
+    g = to_np(got)
+    if rows is not None:
+        g, want = g[rows], want[rows]
+    mx, mean = attn_errors(g, want)
+    assert mx <= MAX_ABS and mean <= MEAN_ABS, (mx, mean)
+    return mx, mean
+
+
+@pytest.mark.parametrize("D", [64, 128])
+@pytest.mark.parametrize("B", [16, 32, 64, 128])
+def test_random_lists(sv, D, B):
+    """Random ascending lists incl. the ragged last KV block, ragged query tiles (N=144)."""
+    sides = [1, 2, 4, 6, 8, 12, 16, 20]          # C = ..., 665, 1065; N_8 = 400
+    K, bh = 8, 3
+    sched, q, k, v = _inputs(sides, K, D, bh, seed=B + D, cap_extra=40)
+    gq, gkv = ceil_div(sched.N(K), B), ceil_div(sched.C(K), B)
+    rng = np.random.default_rng(B)
+    m = rng.random((bh, gq, gkv)) < 0.3
+    m[:, :, gkv - 1] |= rng.random((bh, gq)) < 0.5
+    m[:, :, 0] |= ~m.any(2)
+    rp, ci, st = _lists_from_bool(sv, m)
+    o = sv.block_sparse_attn(sides, K, B, q, k, v, rp, ci)
+    torch.cuda.synchronize()
+    assert st.item() == 0
+    for b in range(bh):
+        want = block_sparse(to_np(q[b]), to_np(k[b]), to_np(v[b]), sched.C(K), B,
+                            merge_lists([m[b]]))
+        _check(o[b], want)
+
+
+@pytest.mark.parametrize("cfg", [TINY, EQ256], ids=["tiny", "256eq"])
+def test_csla_pipeline_small(sv, cfg):
+    """GPU local mask -> GPU lists -> GPU attention vs oracle mask -> oracle attention."""
+    sides, K, B, D, bh = cfg["sides"], cfg["K"], cfg["B"], cfg["D"], cfg["bh"]
+    sched, q, k, v = _inputs(sides, K, D, bh, seed=1)
+    g = sv.geometry(sides, K, B)
+    mask = sv.local_mask(sides, K, B, cfg["sink"], cfg["windows"])
+    rp, ci, st = sv.build_block_lists(bh, g["G_q"], g["G_kv"], [(mask, True)])
+    o = sv.block_sparse_attn(sides, K, B, q, k, v, rp, ci)
+    torch.cuda.synchronize()
+    assert st.item() == 0
+    lists = merge_lists([local_block_mask(sched, K, B, cfg["sink"], cfg["windows"])])
+    for b in range(bh):
+        want = block_sparse(to_np(q[b]), to_np(k[b]), to_np(v[b]), sched.C(K), B, lists)
+        _check(o[b], want)
+
+
+@pytest.mark.parametrize("cfg", [TINY, EQ256], ids=["tiny", "256eq"])
+def test_dense_small(sv, cfg):
+    sides, K, D, bh = cfg["sides"], cfg["K"], cfg["D"], cfg["bh"]
+    sched, q, k, v = _inputs(sides, K, D, bh, seed=2)
+    lse = torch.empty((bh, sched.N(K)), dtype=torch.float32, device="cuda")
+    o = sv.dense_attn(sides, K, q, k, v, lse=lse)
+    torch.cuda.synchronize()
+    for b in range(bh):
+        qb, kb, vb = to_np(q[b]), to_np(k[b]), to_np(v[b])
+        _check(o[b], dense(qb, kb, vb, sched.C(K)))
+        z = qb @ kb[:sched.C(K)].T / np.sqrt(D)
+        ref_lse = np.log(np.exp(z - z.max(1, keepdims=True)).sum(1)) + z.max(1)
+        assert np.abs(lse[b].cpu().numpy() - ref_lse).max() < 1e-3
+
+
+def test_all_blocks_equals_dense_kernel(sv):
+    """An all-ones list through the sparse path == the dense path (same kernel, same order:
+    bitwise equal)."""
+    cfg = EQ256
+    sides, K, B, D, bh = cfg["sides"], cfg["K"], 128, cfg["D"], 2
+    sched, q, k, v = _inputs(sides, K, D, bh, seed=3)
+    gq, gkv = ceil_div(sched.N(K), B), ceil_div(sched.C(K), B)
+    rp, ci, _ = _lists_from_bool(sv, np.ones((bh, gq, gkv), dtype=bool))
+    o1 = sv.block_sparse_attn(sides, K, B, q, k, v, rp, ci)
+    o2 = sv.dense_attn(sides, K, q, k, v)
+    torch.cuda.synchronize()
+    assert torch.equal(o1, o2)
+
+
+def test_full_size_sampled_rows(sv):
+    """2B-shaped config at the bench launch configuration (K=13, B=128, 16 heads, CSLA default):
+    sampled query blocks checked against the oracle one by one."""
+    cfg = INF2B
+    sides, K, B, D, bh = cfg["sides"], cfg["K"], cfg["B"], cfg["D"], cfg["bh"]
+    sched, q, k, v = _inputs(sides, K, D, bh, seed=4)
+    g = sv.geometry(sides, K, B)
+    mask = sv.local_mask(sides, K, B, cfg["sink"], cfg["windows"])
+    rp, ci, st = sv.build_block_lists(bh, g["G_q"], g["G_kv"], [(mask, True)])
+    o = sv.block_sparse_attn(sides, K, B, q, k, v, rp, ci)
+    torch.cuda.synchronize()
+    assert st.item() == 0
+    lists = merge_lists([local_block_mask(sched, K, B, cfg["sink"], cfg["windows"])])
+    rng = np.random.default_rng(0)
+    for b in rng.choice(bh, 4, replace=False):
+        rows_u = sorted(set(rng.choice(g["G_q"], 5, replace=False)) | {0, g["G_q"] - 1})
+        want = block_sparse(to_np(q[b]), to_np(k[b]), to_np(v[b]), sched.C(K), B, lists, rows=rows_u)
+        sel = np.concatenate([np.arange(u * B, min((u + 1) * B, sched.N(K))) for u in rows_u])
+        _check(o[b], want, rows=sel)
+
+
+def test_full_size_dense_sampled(sv):
+    sides, K, D, bh = list(INFINITY_1K_SIDES), 13, 128, 2
+    sched, q, k, v = _inputs(sides, K, D, bh, seed=5)
+    o = sv.dense_attn(sides, K, q, k, v)
+    torch.cuda.synchronize()
+    rows = np.array([0, 1, 777, 2048, 4095])
+    for b in range(bh):
+        want = dense(to_np(q[b])[rows], to_np(k[b]), to_np(v[b]), sched.C(K))
+        mx, mean = attn_errors(to_np(o[b])[rows], want)
+        assert mx <= MAX_ABS and mean <= MEAN_ABS
+
+
+def test_empty_row_gives_zero(sv):
+    sides, K, B, D, bh = [1, 2, 4, 8], 4, 16, 64, 1
+    sched, q, k, v = _inputs(sides, K, D, bh)
+    m = np.zeros((1, 4, 6), dtype=bool)
+    m[0, [0, 1, 3], 2] = True                              # row 2 empty
+    g = sv.geometry(sides, K, B)
+    rp, ci, st = _lists_from_bool(sv, m)
+    lse = torch.empty((1, 64), dtype=torch.float32, device="cuda")
+    o = sv.block_sparse_attn(sides, K, B, q, k, v, rp, ci, lse=lse)
+    torch.cuda.synchronize()
+    assert st.item() == 5
+    assert (o[0, 32:48] == 0).all() and torch.isinf(lse[0, 32:48]).all()
+    assert torch.isfinite(o[0, :32].float()).all()
+
+
+def test_deterministic(sv):
+    cfg = EQ256
+    sides, K, B, D, bh = cfg["sides"], cfg["K"], cfg["B"], cfg["D"], cfg["bh"]
+    sched, q, k, v = _inputs(sides, K, D, bh, seed=6)
+    g = sv.geometry(sides, K, B)
+    mask = sv.local_mask(sides, K, B, cfg["sink"], cfg["windows"])
+    rp, ci, _ = sv.build_block_lists(bh, g["G_q"], g["G_kv"], [(mask, True)])
+    o1 = sv.block_sparse_attn(sides, K, B, q, k, v, rp, ci)
+    o2 = sv.block_sparse_attn(sides, K, B, q, k, v, rp, ci)
+    torch.cuda.synchronize()
+    assert torch.equal(o1, o2)
