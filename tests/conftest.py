@@ -8,6 +8,13 @@ if ROOT not in sys.path:
     sys.path.insert(0, ROOT)
 
 
+def pytest_sessionstart(session):
+    # libsparvar.so is built in-tree before any test imports the binding (it refuses to load
+    # without it); nvcc cross-compiles sm_100a without a GPU.
+    import __graft_entry__
+    __graft_entry__.build()
+
+
 def pytest_configure(config):
     config.addinivalue_line("markers", "gpu: needs a CUDA (sm_100a) device")
     config.addinivalue_line("markers", "slow: long-running CPU test")

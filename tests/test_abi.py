@@ -12,8 +12,8 @@ HEADER = os.path.join(ROOT, "include", "sparvar.h")
 
 @pytest.fixture(scope="module")
 def sv():
-    from paper_2602_04361_b200 import build as b
-    b.build()
+    import __graft_entry__
+    __graft_entry__.build()
     import paper_2602_04361_b200 as pkg
     return pkg
 

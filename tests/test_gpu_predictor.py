@@ -51,10 +51,11 @@ def _margins(mass_row, mode, k, tau, rows_u):
     return np.abs(mass_row - thr) / max(thr, 1e-30)
 
 
+SEED = 11  # standard seed; tests/test_predictor_seeds.py checks it is unambiguous
 CASES = [
     (TINY, 16, 0, 1, 0.0), (TINY, 16, 1, 0, 0.02),
     (EQ256, 32, 0, 2, 0.0), (EQ256, 32, 1, 0, 0.05), (EQ256, 16, 0, 3, 0.0),
-    (INF2B, 128, 0, 5, 0.0), (INF2B, 128, 1, 0, 0.01), (INF2B, 64, 0, 7, 0.0),
+    (INF2B, 128, 0, 5, 0.0), (INF2B, 128, 1, 0, 0.015), (INF2B, 64, 0, 7, 0.0),
 ]
 
 
@@ -63,7 +64,7 @@ def test_predictor_parity(sv, cfg, B, mode, k, tau):
     S, D = cfg["S"], cfg["D"]
     bh = min(cfg["bh"], 4)
     sched = Schedule(cfg["sides"])
-    q, kc = _struct(cfg, 11, bh, S)
+    q, kc = _struct(cfg, SEED, bh, S)
     mask, mass = sv.predict_pattern(cfg["sides"], S, B, cfg["sink"], q, kc, mode, max(k, 1), tau)
     torch.cuda.synchronize()
     gq, gkv = ceil_div(sched.N(S), B), ceil_div(sched.C(S), B)
