@@ -26,7 +26,7 @@ __all__ = [
 ]
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libsparvar.so")
+LIB_PATH = os.environ.get("SPARVAR_LIB") or os.path.join(_HERE, "libsparvar.so")
 
 SELECT_TOPK, SELECT_THRESHOLD = 0, 1
 MAP_FOOTPRINT, MAP_POINT = 0, 1

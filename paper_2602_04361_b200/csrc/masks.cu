@@ -75,6 +75,74 @@ __global__ void local_mask_kernel(const Geo g, int K, int B, int sink_scales, co
 }
 
 // ------------------------------------------------------------------------------------ a4
+// Mapping is a union over tokens, so it is the OR, over the active blocks v of the source row
+// phi(g), of the image T[v] of block v: the target blocks holding a projection of one of v's real
+// tokens.  T depends only on the geometry, not on (b,h) or the row, so each CTA
+// builds T for all source blocks in shared memory, then emits the target rows of its (b,h) range.
+//
+// Token j of source block v: decompose (READING 2), align l' = l + (K - S)
+// (PAPER.md:870), project (READING 14).  A footprint row is a contiguous run of the
+// target scale's row-major layout, marked as one block range.
+__device__ void mark_image(const Geo& g, int j, int shift, int mode, int B, uint32_t* trow) {
+  int l = 1;
+  while (g.cum[l] <= j) ++l;                               // C_{l-1} <= j < C_l
+  const int delta = j - g.cum[l - 1];
+  const int lp = l + shift;
+  const int s = g.side[l - 1], sp = g.side[lp - 1];
+  const int x = delta / s, y = delta % s;
+  const int base = g.cum[lp - 1];
+  if (mode == 1) {                                         // POINT
+    const int xp = x * sp / s, yp = y * sp / s;
+    set_token_range(trow, base + xp * sp + yp, base + xp * sp + yp, B);
+  } else {                                                 // FOOTPRINT (READING 14)
+    const int x0 = x * sp / s, x1 = (x + 1) * sp / s - 1;
+    const int y0 = y * sp / s, y1 = (y + 1) * sp / s - 1;
+    for (int xp = x0; xp <= x1; ++xp)
+      set_token_range(trow, base + xp * sp + y0, base + xp * sp + y1, B);
+  }
+}
+
+__global__ void __launch_bounds__(256) map_table_kernel(const Geo g, int S, int K, int B,
+                                                        int sink_scales, int mode, int G_S,
+                                                        int G_K, int G_kvS, int W_S, int W_K,
+                                                        int bh_total, int bh_per_cta,
+                                                        const uint32_t* __restrict__ src,
+                                                        uint32_t* __restrict__ dst) {
+  extern __shared__ uint32_t table[];                      // [G_kvS][W_K]
+  const int n_kvS = g.cum[S];
+  for (int i = threadIdx.x; i < G_kvS * W_K; i += blockDim.x) table[i] = 0;
+  __syncthreads();
+  for (int j = threadIdx.x; j < n_kvS; j += blockDim.x)
+    mark_image(g, j, K - S, mode, B, table + (j / B) * W_K);
+  __syncthreads();
+  // sink blocks v < ceil(C_sink / B) (READING 13)
+  const int n_sb = sink_scales > 0 ? (g.cum[sink_scales] + B - 1) / B : 0;
+  const int bh0 = blockIdx.x * bh_per_cta;
+  const int bh1 = min(bh_total, bh0 + bh_per_cta);
+  const int items = (bh1 - bh0) * G_K * W_K;
+  for (int it = threadIdx.x; it < items; it += blockDim.x) {
+    const int w = it % W_K;
+    const int gq = (it / W_K) % G_K;
+    const int bh = bh0 + it / (W_K * G_K);
+    int gs = rne_div(2LL * gq * G_S + G_S - G_K, 2LL * G_K);   // phi
+    gs = min(max(gs, 0), G_S - 1);
+    const uint32_t* srow = src + ((long long)bh * G_S + gs) * W_S;
+    uint32_t acc = 0;
+    for (int ws = 0; ws < W_S; ++ws) {
+      uint32_t bits = __ldg(srow + ws);
+      while (bits) {
+        const int v = ws * 32 + __ffs(bits) - 1;
+        bits &= bits - 1;
+        if (v < G_kvS) acc |= table[v * W_K + w];
+      }
+    }
+    const int lo = w * 32;
+    if (lo < n_sb) acc |= (n_sb - lo >= 32) ? 0xffffffffu : ((1u << (n_sb - lo)) - 1u);
+    dst[((long long)bh * G_K + gq) * W_K + w] = acc;
+  }
+}
+
+// Fallback when the block-image table does not fit in shared memory (tiny blocks, e.g. B = 1).
 // One CTA per (target query block gq, bh).  Source row phi(gq); every real token of
 // every active source block is decomposed, aligned to l' = l + (K - S)
 // and projected (READING 14).
@@ -96,24 +164,8 @@ __global__ void map_kernel(const Geo g, int S, int K, int B, int sink_scales, in
     while (bits) {
       const int v = w * 32 + __ffs(bits) - 1;
       bits &= bits - 1;
-      for (int j = v * B + threadIdx.x; j < min((v + 1) * B, n_kvS); j += blockDim.x) {
-        int l = 1;
-        while (g.cum[l] <= j) ++l;                        // C_{l-1} <= j < C_l
-        const int delta = j - g.cum[l - 1];
-        const int lp = l + shift;
-        const int s = g.side[l - 1], sp = g.side[lp - 1];
-        const int x = delta / s, y = delta % s;
-        const int base = g.cum[lp - 1];
-        if (mode == 1) {                                   // POINT
-          const int xp = x * sp / s, yp = y * sp / s;
-          set_token_range(srow, base + xp * sp + yp, base + xp * sp + yp, B);
-        } else {                                           // FOOTPRINT (READING 14)
-          const int x0 = x * sp / s, x1 = (x + 1) * sp / s - 1;
-          const int y0 = y * sp / s, y1 = (y + 1) * sp / s - 1;
-          for (int xp = x0; xp <= x1; ++xp)
-            set_token_range(srow, base + xp * sp + y0, base + xp * sp + y1, B);
-        }
-      }
+      for (int j = v * B + threadIdx.x; j < min((v + 1) * B, n_kvS); j += blockDim.x)
+        mark_image(g, j, shift, mode, B, srow);
     }
   }
   if (threadIdx.x == 0 && sink_scales > 0) set_token_range(srow, 0, g.cum[sink_scales] - 1, B);
@@ -123,10 +175,11 @@ __global__ void map_kernel(const Geo g, int S, int K, int B, int sink_scales, in
 }
 
 // ------------------------------------------------------------------------------------ a5
-// Single CTA of 1024 threads.  Phase 1: popcount of every OR-ed row -> row_ptr[r+1].  Phase 2:
-// block-wide exclusive scan over rows.  Phase 3: each warp compacts its rows: lane = word, warp
-// exclusive scan of popcounts (shuffle) gives each word's output offset, bits are emitted in
-// ascending order.
+// Single CTA of 1024 threads, one THREAD per row (rows are a few words wide), rows processed in
+// chunks of 1024 with a running carry.  Pass 1: OR the masks' words, popcount, block-wide
+// exclusive scan -> row_ptr.  Pass 2: every thread re-reads its row's words (L1/L2 hits) and
+// writes its set bits in ascending order at row_ptr[r].  All loads of a chunk are in flight at
+// once, so the kernel costs a few memory latencies per chunk.
 __device__ __forceinline__ uint32_t row_word(const MaskSet& ms, int r, int u, int w, int W) {
   uint32_t x = 0;
   for (int i = 0; i < ms.n; ++i)
@@ -146,22 +199,17 @@ __global__ void __launch_bounds__(1024) build_lists_kernel(int rows, int g_q, in
   if (threadIdx.x == 0) {
     s_carry = 0;
     s_err = 0;
-  }
-  // phase 1
-  for (int r = warp; r < rows; r += nw) {
-    const int u = r % g_q;
-    int c = 0;
-    for (int w = lane; w < W; w += 32) c += __popc(row_word(ms, r, u, w, W));
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
-    if (lane == 0) row_ptr[r + 1] = c;
+    row_ptr[0] = 0;
   }
   __syncthreads();
-  // phase 2 (threads own consecutive rows of a 1024-row chunk)
   for (int base = 0; base < rows; base += blockDim.x) {
     const int r = base + threadIdx.x;
-    const int c = r < rows ? row_ptr[r + 1] : 0;
-    if (r < rows && c == 0) s_err = 5;
+    int c = 0;
+    if (r < rows) {
+      const int u = r % g_q;
+      for (int w = 0; w < W; ++w) c += __popc(row_word(ms, r, u, w, W));
+      if (c == 0) s_err = 5;                               // SPARVAR_ERR_EMPTY_ROW
+    }
     int inc = c;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
@@ -180,41 +228,27 @@ __global__ void __launch_bounds__(1024) build_lists_kernel(int rows, int g_q, in
       s_warp[lane] = wv;
     }
     __syncthreads();
-    const int carry = s_carry;
-    const int pre = (warp > 0 ? s_warp[warp - 1] : 0) + carry;
+    const int pre = (warp > 0 ? s_warp[warp - 1] : 0) + s_carry;
     if (r < rows) row_ptr[r + 1] = pre + inc;
     __syncthreads();
     if (threadIdx.x == blockDim.x - 1) s_carry = pre + inc;
     __syncthreads();
   }
-  if (threadIdx.x == 0) row_ptr[0] = 0;
   const long long nnz = s_carry;
   if (nnz > cap) {
-    if (threadIdx.x == 0 && status) atomicCAS(status, 0, 4);
+    if (threadIdx.x == 0 && status) atomicCAS(status, 0, 4);   // SPARVAR_ERR_CAPACITY
     return;
   }
   if (threadIdx.x == 0 && status && s_err) atomicCAS(status, 0, s_err);
-  __syncthreads();
-  // phase 3
-  for (int r = warp; r < rows; r += nw) {
+  for (int r = threadIdx.x; r < rows; r += blockDim.x) {
     const int u = r % g_q;
-    int off = row_ptr[r];
-    for (int w0 = 0; w0 < W; w0 += 32) {
-      const int w = w0 + lane;
-      uint32_t x = w < W ? row_word(ms, r, u, w, W) : 0u;
-      const int c = __popc(x);
-      int inc = c;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const int t = __shfl_up_sync(0xffffffffu, inc, o);
-        if (lane >= o) inc += t;
-      }
-      int pos = off + inc - c;
+    int pos = row_ptr[r];
+    for (int w = 0; w < W; ++w) {
+      uint32_t x = row_word(ms, r, u, w, W);
       while (x) {
         col_idx[pos++] = w * 32 + __ffs(x) - 1;
         x &= x - 1;
       }
-      off += __shfl_sync(0xffffffffu, inc, 31);
     }
   }
 }
@@ -245,19 +279,33 @@ cudaError_t launch_map_indices(const Geo& g, int S, int K, int block, int sink_s
                                int bh, const uint32_t* src, uint32_t* dst, cudaStream_t st) {
   const int nS = g.side[S - 1] * g.side[S - 1], nK = g.side[K - 1] * g.side[K - 1];
   const int G_S = (nS + block - 1) / block, G_K = (nK + block - 1) / block;
-  const int W_S = ((g.cum[S] + block - 1) / block + 31) / 32;
+  const int G_kvS = (g.cum[S] + block - 1) / block;
+  const int W_S = (G_kvS + 31) / 32;
   const int W_K = ((g.cum[K] + block - 1) / block + 31) / 32;
-  const size_t smem = size_t(W_K) * 4;
-  if (smem > 200 * 1024) return cudaErrorInvalidValue;
+  const size_t smem = size_t(G_kvS) * W_K * 4;
+  if (smem > 100 * 1024) {
+    const size_t row_smem = size_t(W_K) * 4;
+    if (row_smem > 200 * 1024) return cudaErrorInvalidValue;
+    if (row_smem > 48 * 1024) {
+      cudaError_t e = cudaFuncSetAttribute(map_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           (int)row_smem);
+      if (e != cudaSuccess) return e;
+    }
+    dim3 grid(G_K, bh);
+    map_kernel<<<grid, block >= 128 ? 128 : 64, row_smem, st>>>(g, S, K, block, sink_scales, mode,
+                                                                G_S, G_K, W_S, W_K, src, dst);
+    return cudaGetLastError();
+  }
   if (smem > 48 * 1024) {
-    cudaError_t e = cudaFuncSetAttribute(map_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)smem);
+    cudaError_t e = cudaFuncSetAttribute(map_table_kernel,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
   }
-  dim3 grid(G_K, bh);
-  const int threads = block >= 128 ? 128 : 64;
-  map_kernel<<<grid, threads, smem, st>>>(g, S, K, block, sink_scales, mode, G_S, G_K, W_S, W_K,
-                                          src, dst);
+  // Enough CTAs to cover the SMs; each CTA rebuilds the (identical) table for its (b,h) range.
+  const int bh_per_cta = bh <= 148 ? 1 : (bh + 147) / 148;
+  const int ctas = (bh + bh_per_cta - 1) / bh_per_cta;
+  map_table_kernel<<<ctas, 256, smem, st>>>(g, S, K, block, sink_scales, mode, G_S, G_K, G_kvS,
+                                            W_S, W_K, bh, bh_per_cta, src, dst);
   return cudaGetLastError();
 }
 

@@ -1,0 +1,50 @@
+"""Development aid: softmax phase timings (SM clocks) from a -DSV_PROF variant library.
+    SPARVAR_LIB=variants/lib_prof.so python scripts/prof_phases.py [csla|cs4a|dense]"""
+import ctypes
+import os
+import sys
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np
+import torch
+import paper_2602_04361_b200 as sv
+
+which = sys.argv[1] if len(sys.argv) > 1 else "csla"
+sides = [1, 2, 4, 6, 8, 12, 16, 20, 24, 32, 40, 48, 64]
+K, S, B, D, bh = 13, 11, 128, 128, 96
+q = torch.randn(bh, 4096, D, device="cuda").bfloat16()
+qS = torch.randn(bh, 1600, D, device="cuda").bfloat16()
+k = torch.randn(bh, 10521, D, device="cuda").bfloat16()
+v = torch.randn(bh, 10521, D, device="cuda").bfloat16()
+layer = sv.SparseLayer(sides, K, S, B, bh, sink_scales=5, topk=5)
+layer.build_patterns(qS, k)
+fn = (lambda: sv.dense_attn(sides, K, q, k, v)) if which == "dense" else \
+     (lambda: layer.attend(which, q, k, v))
+for _ in range(3):
+    fn()
+torch.cuda.synchronize()
+buf = (ctypes.c_longlong * 8192)()
+sv.lib.sparvar_prof_read.argtypes = [ctypes.c_void_p, ctypes.c_int]
+sv.lib.sparvar_prof_read(buf, 8192)
+a = np.array(buf[:], dtype=np.int64)
+n = int((a != 0).sum() // 5)
+st = a[:5 * n].reshape(n, 5)
+st = st[st[:, 0] > 0]
+d = np.diff(st, axis=1)
+gap = st[1:, 0] - st[:-1, 4]
+print(f"{which}: steps recorded {len(st)}")
+print("median clk: wait %.0f  pass1(max) %.0f  pass2(exp) %.0f  tail %.0f  gap->next %.0f  period %.0f" % (
+    np.median(d[:, 0]), np.median(d[:, 1]), np.median(d[:, 2]), np.median(d[:, 3]), np.median(gap),
+    np.median(np.diff(st[:, 0]))))
+print("first 12 steps (wait, pass1, pass2, tail):")
+print(d[:12])
+
+mm = a[4096:4096 + 6 * 682].reshape(-1, 6)
+mm = mm[(mm[:, 0] > 0) & (mm[:, 5] > 0)]
+if len(mm):
+    dm = np.diff(mm, axis=1)
+    print("MMA slot0 median clk: p_wait %.0f  V_ready %.0f  PV_issue %.0f  K_ready %.0f  QK_issue %.0f" %
+          tuple(np.median(dm, axis=0)))
+    print(dm[:8])
+
+pv = a[4096 + 4010:4096 + 4018]; qk = a[4096 + 4000:4096 + 4008]
+print("per-MMA issue deltas PV:", np.diff(pv), " QK:", np.diff(qk))

@@ -168,3 +168,44 @@ def test_deterministic(sv):
     o2 = sv.block_sparse_attn(sides, K, B, q, k, v, rp, ci)
     torch.cuda.synchronize()
     assert torch.equal(o1, o2)
+
+
+@pytest.mark.parametrize("B", [128, 64])
+def test_persistent_schedule_mixed_lengths(sv, B):
+    """Many tiles per CTA with very uneven list lengths (1 block up to every block, plus empty
+    rows): exercises the persistent two-slot schedule, the Q-buffer rotation and the KV ring
+    wrap-around at the full Infinity-1K shape.  Sampled query blocks vs the oracle."""
+    sides, K, D, bh = list(INFINITY_1K_SIDES), 13, 128, 40
+    sched, q, k, v = _inputs(sides, K, D, bh, seed=7)
+    gq, gkv = ceil_div(sched.N(K), B), ceil_div(sched.C(K), B)
+    rng = np.random.default_rng(11)
+    kind = rng.integers(0, 5, size=(bh, gq))
+    m = np.zeros((bh, gq, gkv), dtype=bool)
+    for b in range(bh):
+        for u in range(gq):
+            if kind[b, u] == 0:
+                m[b, u, rng.integers(0, gkv)] = True            # a single block
+            elif kind[b, u] == 1:
+                m[b, u, :] = True                                # every block
+            elif kind[b, u] == 2:
+                m[b, u, :] = rng.random(gkv) < 0.1
+            elif kind[b, u] == 3:
+                m[b, u, gkv - 1] = True                          # only the ragged last block
+            # kind 4: empty row
+    rp, ci, st = _lists_from_bool(sv, m)
+    lse = torch.empty((bh, sched.N(K)), dtype=torch.float32, device="cuda")
+    o = sv.block_sparse_attn(sides, K, B, q, k, v, rp, ci, lse=lse)
+    torch.cuda.synchronize()
+    assert st.item() in (0, 5)
+    for b in rng.choice(bh, 6, replace=False):
+        rows_u = sorted(set(rng.choice(gq, 6, replace=False)) | {0, gq - 1})
+        empty = [u for u in rows_u if not m[b, u].any()]
+        live = [u for u in rows_u if m[b, u].any()]
+        for u in empty:
+            assert (o[b, u * B:(u + 1) * B] == 0).all()
+            assert torch.isinf(lse[b, u * B:(u + 1) * B]).all()
+        if live:
+            want = block_sparse(to_np(q[b]), to_np(k[b]), to_np(v[b]), sched.C(K), B,
+                                merge_lists([m[b]]), rows=live)
+            sel = np.concatenate([np.arange(u * B, min((u + 1) * B, sched.N(K))) for u in live])
+            _check(o[b], want, rows=sel)
