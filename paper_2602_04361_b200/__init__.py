@@ -50,10 +50,10 @@ class _Shape(ctypes.Structure):
                 ("o_stride_bh", ctypes.c_int64)]
 
 
-def _load():
-    if not os.path.exists(LIB_PATH):
-        raise ImportError(f"{LIB_PATH} not built: run `python -m paper_2602_04361_b200.build`")
-    L = ctypes.CDLL(LIB_PATH)
+def _load(path: str = LIB_PATH):
+    if not os.path.exists(path):
+        raise ImportError(f"{path} not built: run `python -m paper_2602_04361_b200.build`")
+    L = ctypes.CDLL(path)
     P, I32, I64, F32 = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64, ctypes.c_float
     S = ctypes.POINTER(_Schedule)
     SH = ctypes.POINTER(_Shape)

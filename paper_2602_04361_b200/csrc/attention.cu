@@ -4,29 +4,29 @@
 // real tokens J of the KV blocks listed for u (PAPER.md:204-212 Eq. attn_cross_scale,
 // PAPER.md:318-328 Eq. sparse_update, PAPER.md:397-407 Eq. block_mask; READINGS 9, 17, 20).
 //
-// Design (DESIGN.md §7 "attn_fwd_kernel v1"):
-//  * Persistent: one CTA per SM (512 TMEM columns), CTA c walks the 128-row query tiles
-//    ("items", (b,h)-major) c, c+grid, ...  Two tile SLOTS run concurrently in a CTA, each with
-//    its own S/P (128 TMEM cols) and O (D cols) accumulators and its own softmax warpgroup, so
-//    the tensor core works on one slot while the other slot's softmax runs (ping-pong).
-//  * The MMA warp issues in a fixed round-robin order: per round and slot, O += P_j V_j then
-//    S = Q K_{j+1}^T (or the next tile's first S).  Every role (KV loader, Q loader, MMA, softmax)
-//    derives the same order from a per-CTA schedule built once in shared memory, so a single KV
-//    ring (TMA, mbarrier full/empty) serves both slots and no role needs to talk to another
-//    except through the ring / tile barriers.
-//  * Q lives in 3 shared buffers: two slots' current tiles plus one prefetched tile.  A buffer is
-//    released by the commit of its tile's last Q K^T, and the schedule assigns each new tile the
-//    earliest pending release (deadlock-free: that release precedes the tile's start in the MMA
-//    order).
+// Design (DESIGN.md §7 "attn_fwd_kernel"):
+//  * Persistent, one CTA per SM (all 512 TMEM columns).  The 128-row query tiles ("items",
+//    (b,h)-major) are split into CONTIGUOUS per-CTA ranges of equal cost (cost = listed blocks +
+//    a per-tile overhead), found by a warp-parallel search over row_ptr (the CSR prefix sums).
+//  * Two tile SLOTS per CTA, each with its own S/P (128 TMEM cols) and O (D cols) accumulators
+//    and its own softmax warpgroup: the tensor core works on one slot while the other slot's
+//    softmax runs.  The MMA warp issues in a fixed round-robin order (per round and slot:
+//    O += P_j V_j in two halves, then S = Q K_{j+1}^T or the next tile's first S), and every role
+//    derives the same order from a per-CTA schedule (thread 0 simulates the round-robin once per
+//    batch of up to MAX_TILES tiles), so one KV ring serves both slots.
+//  * Q lives in 3 shared buffers (two current tiles + one prefetched); a buffer is released by
+//    the commit of its tile's last Q K^T and the schedule gives each new tile the earliest
+//    pending release (that release precedes the tile's first MMA, so no deadlock).
 //  * S (fp32) and O (fp32) live in TMEM; P (bf16) overwrites S in place and is the TMEM A operand
-//    of the P.V MMA (tcgen05 ops of one thread execute in issue order, so the next S = Q K^T issued
-//    after P.V cannot clobber P early).  Online softmax in fp32, exp2 domain, with a lazy rescale
-//    of O (only when the running max grows by more than 2^8).  The commit that signals S_j also
-//    covers P_{j-1} V_{j-1}, so a rescale of O never races the tensor core.
+//    of P.V (tcgen05 ops of one thread execute in issue order, so the next Q K^T cannot clobber P
+//    early).  fp32 online softmax in the exp2 domain with lazy rescale of O (only when the running
+//    max grows by more than 2^8); the S_j commit also covers P_{j-1} V_{j-1}.
+//  * A separate epilogue warpgroup drains each finished tile (TMEM O -> 1/l -> bf16 -> global,
+//    LSE) in completion order, so the softmax warpgroup starts the slot's next tile at once; the
+//    next tile's first P.V waits on "O drained".
 //  * Block sizes below 128: a 128-row tile holds G = 128/B query blocks; the KV steps are the
-//    ascending union of their lists and each row masks the steps its own block does not list, so
-//    every row sees exactly its own list.  The ragged last KV block is masked to -inf
-//    (READING 20): TMA zero fill alone would give logit 0.
+//    ascending union of their lists and each row masks the steps its own block does not list.
+//    The ragged last KV block is masked to -inf (READING 20): TMA zero fill alone gives logit 0.
 #include <cuda_bf16.h>
 #include <cstdio>
 
@@ -34,55 +34,70 @@
 #include "ptx.cuh"
 
 #ifdef SV_PROF
-// Development instrumentation (built only into variant libraries, scripts/build_variant.sh):
-// globaltimer-free SM clock stamps of the softmax phases of CTA 0 / slot 0 / row 0.
+// Development instrumentation (variant libraries only, scripts/build_variant.sh).
 __device__ long long sv_prof_buf[8192];
 extern "C" int sparvar_prof_read(long long* host, int n) {
   return cudaMemcpyFromSymbol(host, sv_prof_buf, sizeof(long long) * n) == cudaSuccess ? 0 : 1;
 }
-#define SV_STAMP(slot_, i_) \
-  if (blockIdx.x == 0 && threadIdx.x == 0 && (i_) < 8192) sv_prof_buf[(i_)] = clock64();
-#define SV_STAMP_MMA(i_) \
-  if (blockIdx.x == 0 && (i_) < 4096) sv_prof_buf[4096 + (i_)] = clock64();
+#define SV_STAMP(i_) \
+  if (blockIdx.x == 0 && threadIdx.x == 0 && (i_) < 7000) sv_prof_buf[(i_)] = clock64();
+#define SV_STAMP_CTA(base_) \
+  if (threadIdx.x == 0 && blockIdx.x < 192) sv_prof_buf[(base_) + blockIdx.x] = (long long)globaltimer_ns();
 #else
-#define SV_STAMP(slot_, i_)
-#define SV_STAMP_MMA(i_)
+#define SV_STAMP(i_)
+#define SV_STAMP_CTA(base_)
+#endif
+
+#ifndef SV_EMU_EVERY
+#define SV_EMU_EVERY 0
 #endif
 
 namespace sv {
 namespace {
 
 constexpr int BM = 128;                  // query rows per tile (TMEM lanes)
-constexpr int NUM_WARPS = 12;            // WG0 softmax slot 0, WG1 softmax slot 1, WG2: MMA, KV, Q, idle
+constexpr int NUM_WARPS = 16;            // WG0/WG1 softmax slot 0/1, WG2 MMA/KV/Q/zero, WG3 epilogue
 constexpr int NUM_THREADS = NUM_WARPS * 32;
-constexpr int WARP_MMA = 8, WARP_KV = 9, WARP_Q = 10;
-// setmaxnreg moves registers inside the CTA's own pool (launch: 12 warps x 168): the 8 softmax warps
-// take 8 x 56 more, the 4 other warps give 4 x 112 back.
-constexpr int REG_LAUNCH = 168;
-constexpr int REG_SOFTMAX = 224;
-constexpr int REG_OTHER = 56;
-static_assert(8 * (REG_SOFTMAX - REG_LAUNCH) <= 4 * (REG_LAUNCH - REG_OTHER), "register pool");
-#ifndef SV_EMU_EVERY
-#define SV_EMU_EVERY 4
-#endif
+constexpr int WARP_MMA = 8, WARP_KV = 9, WARP_Q = 10, WARP_ZERO = 11, WARP_EPI = 12;
+// setmaxnreg moves registers inside the CTA's own pool (launch: 16 warps x 128): the 8 softmax
+// warps take 8 x 72 more, WG2 gives 4 x 64 and WG3 4 x 80 back.
+constexpr int REG_LAUNCH = 128;
+constexpr int REG_SOFTMAX = 200;
+constexpr int REG_PRODUCER = 64;         // WG2: MMA issuer, loaders
+constexpr int REG_EPILOGUE = 48;         // WG3
+static_assert(8 * (REG_SOFTMAX - REG_LAUNCH) <=
+                  4 * (REG_LAUNCH - REG_PRODUCER) + 4 * (REG_LAUNCH - REG_EPILOGUE),
+              "register pool");
 constexpr int EMU_EVERY = SV_EMU_EVERY;  // 1 in EMU_EVERY exp2 pairs on the FMA pipe (0 = none)
 constexpr uint32_t TMEM_COLS = 512;
 constexpr int NQB = 3;                   // Q buffers
-constexpr int MAX_TILES = 128;           // tiles per CTA per launch (the host splits bigger jobs)
+constexpr int MAX_TILES = 96;            // tiles per schedule batch
+constexpr int TILE_OVERHEAD = 2;         // per-tile cost, in KV steps, for the balanced partition
 constexpr int SMEM_LIMIT = 232448;       // 227 KB opt-in
-constexpr int SMEM_SMALL = 1600;         // schedule + barriers
-constexpr int SMEM_SLACK = 1024;         // alignment of the dynamic smem base to 1024
+constexpr uint8_t EMPTY_TILE = 0xFF;
+
+// Small shared state after the Q / KV buffers.
+struct Small {
+  float2 stats[2][BM];          // per slot, per row: (1/l or 0, lse) handed softmax -> epilogue
+  uint16_t n[MAX_TILES];        // KV steps of the batch's i-th tile
+  uint8_t meta[MAX_TILES];      // slot | buf << 1 | (use parity of buf) << 3, or EMPTY_TILE
+  uint8_t eord[MAX_TILES];      // completion order (for the epilogue)
+  int T, Tn, lo, hi, uses;
+  uint32_t tmem_slot;
+  uint64_t bars[2 * NQB + 2 * 8 + 14];
+};
 
 template <int D, int BLK>
 struct Cfg {
   static constexpr int NBOX = D / 64;                       // 64-element (128 B) TMA boxes per row
   static constexpr int Q_BYTES = BM * D * 2;
   static constexpr int STAGE_BYTES = BLK * D * 2;
-  static constexpr int AVAIL = SMEM_LIMIT - SMEM_SMALL - SMEM_SLACK - NQB * Q_BYTES;
+  static constexpr int AVAIL = SMEM_LIMIT - (int)sizeof(Small) - NQB * Q_BYTES;
   static constexpr int NST = AVAIL / STAGE_BYTES > 8 ? 8 : AVAIL / STAGE_BYTES;
   static constexpr int G = BM / BLK;                        // query blocks per tile
-  static constexpr int SMEM = SMEM_SLACK + NQB * Q_BYTES + NST * STAGE_BYTES + SMEM_SMALL;
+  static constexpr int SMEM = NQB * Q_BYTES + NST * STAGE_BYTES + (int)sizeof(Small);
   static_assert(NST >= 2, "KV ring too small");
+  static_assert(NST <= 8, "barrier array sized for 8 stages");
 };
 
 // Enumerates the KV steps of a tile: ascending union of the lists of its G query blocks, with
@@ -148,19 +163,6 @@ struct Steps {
     return n;
   }
 };
-
-// Per-CTA schedule in shared memory.  ord[k] (k = start order) indexes the CTA's non-empty tiles;
-// meta[k] = slot | buf << 1 | (use parity of buf) << 3.
-struct Sched {
-  int item[MAX_TILES];     // global item id of the CTA's i-th tile (CTA order)
-  int n[MAX_TILES];        // KV steps of that tile
-  uint8_t ord[MAX_TILES];  // start order -> CTA-order index
-  uint8_t meta[MAX_TILES];
-  int T;                   // tiles of this CTA
-  int Tn;                  // non-empty tiles
-};
-static_assert(((sizeof(Sched) + 15) & ~15ull) + 8 * (2 * NQB + 2 * 8 + 6) + 16 <= SMEM_SMALL,
-              "schedule + barriers exceed SMEM_SMALL");
 
 __device__ __forceinline__ bool elect_one() {
   uint32_t pred;
@@ -229,6 +231,18 @@ __device__ __forceinline__ void ex2_emu2(uint64_t x2, float& p0, float& p1) {
   p1 = __int_as_float(__float_as_int(q1) + (__float_as_int(t1) << 23));
 }
 
+// Cost prefix F(i) of the first i items of [item_begin, item_end) (monotone in i): listed blocks
+// (row_ptr prefix sums) + TILE_OVERHEAD per tile.
+template <int G>
+__device__ __forceinline__ long long cost_prefix(const AttnArgs& a, int item_begin, int i,
+                                                 int n_tiles, int g_kv, int base_row) {
+  if (a.row_ptr == nullptr) return (long long)(g_kv + TILE_OVERHEAD) * i;
+  const int item = item_begin + i;
+  const int bh = item / n_tiles, tile = item % n_tiles;
+  const int row = bh * a.g_q + min(tile * G, a.g_q);
+  return (long long)(__ldg(a.row_ptr + row) - base_row) + (long long)TILE_OVERHEAD * i;
+}
+
 template <int D, int BLK>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
 attn_fwd_kernel(const __grid_constant__ CUtensorMap tmap_q,
@@ -237,30 +251,33 @@ attn_fwd_kernel(const __grid_constant__ CUtensorMap tmap_q,
                 int item_end) {
   using C = Cfg<D, BLK>;
   constexpr int G = C::G;
-  extern __shared__ __align__(1024) uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
-                                             ~uintptr_t(1023));
+  extern __shared__ __align__(1024) uint8_t smem[];
   uint8_t* sQ = smem;                                       // NQB x Q_BYTES
   uint8_t* sKV = smem + NQB * C::Q_BYTES;                   // NST x STAGE_BYTES
-  Sched* sch = reinterpret_cast<Sched*>(sKV + C::NST * C::STAGE_BYTES);
-  uint64_t* bars = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(sch) +
-                                               ((sizeof(Sched) + 15) & ~size_t(15)));
-  uint64_t* q_full = bars;                 // [NQB]
-  uint64_t* q_empty = bars + NQB;          // [NQB]
-  uint64_t* kv_full = bars + 2 * NQB;      // [NST]
-  uint64_t* kv_empty = kv_full + C::NST;   // [NST]
-  uint64_t* s_bar = kv_empty + C::NST;     // [2] S_j of slot ready (also covers P_{j-1}V_{j-1})
-  uint64_t* p_bar = s_bar + 2;             // [2] P_j of slot written (128 arrivals)
-  uint64_t* o_bar = p_bar + 2;             // [2] last P.V of a slot's tile complete
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_bar + 2);
+  Small* sm = reinterpret_cast<Small*>(sKV + C::NST * C::STAGE_BYTES);
+  uint64_t* q_full = sm->bars;             // [NQB] Q tile landed
+  uint64_t* q_empty = q_full + NQB;        // [NQB] last Q K^T of the buffer's tile complete
+  uint64_t* kv_full = q_empty + NQB;       // [NST]
+  uint64_t* kv_empty = kv_full + 8;        // [NST]
+  uint64_t* s_bar = kv_empty + 8;          // [2] S_j of slot ready (also covers P_{j-1}V_{j-1})
+  uint64_t* p_bar = s_bar + 2;             // [2][2] first / second half of P_j written (128)
+  uint64_t* o_bar = p_bar + 4;             // [2] last P.V of the slot's tile complete
+  uint64_t* o_free = o_bar + 2;            // [2] epilogue drained O of the slot (128)
+  uint64_t* st_bar = o_free + 2;           // [2] softmax wrote the tile's row stats (128)
+  uint64_t* st_free = st_bar + 2;          // [2] epilogue read them (128)
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   const int g_kv = (a.n_kv + BLK - 1) / BLK;
   const int n_tiles = (a.n_q + BM - 1) / BM;
+  SV_STAMP_CTA(7400)
 
   // ------------------------------------------------------------------ setup
   if (threadIdx.x == 0) {
+    if ((smem_u32(smem) & 1023u) != 0) {
+      printf("sparvar: dynamic shared memory not 1024-byte aligned\n");
+      __trap();
+    }
     for (int i = 0; i < NQB; ++i) {
       mbar_init(q_full + i, 1);
       mbar_init(q_empty + i, 1);
@@ -271,9 +288,14 @@ attn_fwd_kernel(const __grid_constant__ CUtensorMap tmap_q,
     }
     for (int t = 0; t < 2; ++t) {
       mbar_init(s_bar + t, 1);
-      mbar_init(p_bar + t, BM);
+      mbar_init(p_bar + 2 * t, BM);
+      mbar_init(p_bar + 2 * t + 1, BM);
       mbar_init(o_bar + t, 1);
+      mbar_init(o_free + t, BM);
+      mbar_init(st_bar + t, BM);
+      mbar_init(st_free + t, BM);
     }
+    sm->uses = 0;
     fence_barrier_init();
   }
   if (warp == WARP_KV && lane == 0) {
@@ -282,407 +304,520 @@ attn_fwd_kernel(const __grid_constant__ CUtensorMap tmap_q,
   }
   if (warp == WARP_Q && lane == 0) prefetch_tmap(&tmap_q);
   if (warp == WARP_MMA) {
-    tmem_alloc(tmem_slot, TMEM_COLS);
+    tmem_alloc(&sm->tmem_slot, TMEM_COLS);
     tmem_relinquish();
   }
-  // tile lengths, in parallel
-  int T = 0;
-  {
-    const int first = item_begin + blockIdx.x;
-    if (first < item_end) T = (item_end - first + gridDim.x - 1) / gridDim.x;
-    for (int i = threadIdx.x; i < T; i += NUM_THREADS) {
-      const int it = first + i * gridDim.x;
-      Steps<G> st;
-      st.init(a, it / n_tiles, it % n_tiles, g_kv);
-      sch->item[i] = it;
-      sch->n[i] = st.count(a);
+  if (warp == 1) {
+    // balanced contiguous range [lo, hi) of this CTA: lanes 0-15 search the lower boundary,
+    // lanes 16-31 the upper one, 16 probes per round (min i with F(i) >= target)
+    const int N = item_end - item_begin;
+    const int base_row =
+        a.row_ptr == nullptr ? 0
+                             : __ldg(a.row_ptr + (item_begin / n_tiles) * a.g_q +
+                                     min((item_begin % n_tiles) * G, a.g_q));
+    const long long total = cost_prefix<G>(a, item_begin, N, n_tiles, g_kv, base_row);
+    const int half = lane >> 4, hl = lane & 15;
+    const int c = blockIdx.x + half;
+    const long long target = total * c / (long long)gridDim.x;
+    int lo = -1, hi = N;                   // F(lo) < target <= F(hi)  (F(-1) = -inf)
+    if (c == 0) hi = 0;
+    if (c == (int)gridDim.x) lo = N - 1;
+    while (__any_sync(0xffffffffu, hi - lo > 1)) {
+      const int span = hi - lo;
+      const int p = lo + (int)(((long long)span * (hl + 1)) / 17);
+      const bool ok = span > 1 && p > lo && p < hi &&
+                      cost_prefix<G>(a, item_begin, p, n_tiles, g_kv, base_row) >= target;
+      const uint32_t m = __ballot_sync(0xffffffffu, ok) >> (half * 16) & 0xFFFFu;
+      if (span > 1) {
+        if (m != 0) {
+          const int f = __ffs(m) - 1;
+          hi = lo + (int)(((long long)span * (f + 1)) / 17);
+          if (f > 0) lo = lo + (int)(((long long)span * f) / 17);
+        } else {
+          lo = lo + (int)(((long long)span * 16) / 17);
+        }
+      }
+    }
+    const int lo_res = __shfl_sync(0xffffffffu, hi, 0);
+    const int hi_res = __shfl_sync(0xffffffffu, hi, 16);
+    if (lane == 0) {
+      sm->lo = item_begin + lo_res;
+      sm->hi = item_begin + hi_res;
     }
   }
   tc_fence_before();
   __syncthreads();
-  // round-robin simulation of the MMA order -> slot, Q buffer and start order of every tile
-  if (threadIdx.x == 0) {
-    long long fin_key[2] = {0, 0};   // key of the op that finishes the slot's current tile
-    int round_end[2] = {0, 0};       // round at which the slot's current tile finishes
-    bool busy[2] = {false, false};
-    int pend_key[NQB + 1], pend_buf[NQB + 1], npend = 0;
-    int uses[NQB] = {0, 0, 0};
-    int k = 0;
-    for (int i = 0; i < T; ++i) {
-      const int n = sch->n[i];
-      if (n == 0) continue;
-      int slot, R;
-      if (k < 2) {
-        slot = k;
-        R = -1;
-      } else {
-        slot = (!busy[1] || (busy[0] && fin_key[0] < fin_key[1])) ? 0 : 1;
-        R = round_end[slot];
-      }
-      int buf;
-      if (k < NQB) {
-        buf = k;
-      } else {
-        int best = 0;
-        for (int p = 1; p < npend; ++p)
-          if (pend_key[p] < pend_key[best]) best = p;
-        buf = pend_buf[best];
-        pend_key[best] = pend_key[npend - 1];
-        pend_buf[best] = pend_buf[npend - 1];
-        --npend;
-      }
-      // op (round r, slot s) has key 2*(r+1)+s; last Q K^T at round R+n-1, last P.V at R+n
-      pend_key[npend] = 2 * (R + n) + slot;
-      pend_buf[npend] = buf;
-      ++npend;
-      busy[slot] = true;
-      round_end[slot] = R + n;
-      fin_key[slot] = 2LL * (R + n + 1) + slot;
-      sch->ord[k] = (uint8_t)i;
-      sch->meta[k] = (uint8_t)(slot | (buf << 1) | ((uses[buf] & 1) << 3));
-      ++uses[buf];
-      ++k;
-    }
-    sch->T = T;
-    sch->Tn = k;
-  }
-  __syncthreads();
   tc_fence_after();
-  const uint32_t tmem = *tmem_slot;
-  const int Tn = sch->Tn;
+  const uint32_t tmem = sm->tmem_slot;
+  const int range_lo = sm->lo, range_hi = sm->hi;
+  SV_STAMP_CTA(7600)
 
-  if (warp >= 8) {
-  reg_dealloc<REG_OTHER>();
-  if (warp == WARP_KV) {
-    // ---------------------------------------------------------------- KV loader
-    if (lane == 0) {
-      const uint64_t pol = policy_evict_last();
-      int kcur[2] = {-1, -1};
-      int jn[2] = {0, 0}, nn[2] = {0, 0}, vcur[2] = {0, 0}, bhs[2] = {0, 0};
-      Steps<G> st[2];
-      int idx = 0;
-      auto load = [&](const CUtensorMap* m, int v, int bh) {
-        const int s = idx % C::NST;
-        const uint32_t ph = (idx / C::NST) & 1;
-        ++idx;
-        mbar_wait(kv_empty + s, ph ^ 1);
-        uint8_t* dst = sKV + s * C::STAGE_BYTES;
-        mbar_arrive_expect_tx(kv_full + s, C::STAGE_BYTES);
+  // role state that persists across schedule batches (barrier phases, ring positions)
+  int kv_idx = 0;                  // KV loader / MMA: ring position
+  uint32_t p_cnt0 = 0, p_cnt1 = 0; // MMA: P phases consumed per slot
+  int tiles0 = 0, tiles1 = 0;      // MMA / softmax / epilogue: tiles done per slot
+  uint32_t s_cnt = 0;              // softmax: S phases consumed
+  uint32_t q_used = 0;             // Q loader: buffers used at least once (bits)
+
+  for (int b0 = range_lo; b0 < range_hi; b0 += MAX_TILES) {
+    const int T = min(MAX_TILES, range_hi - b0);
+    for (int i = threadIdx.x; i < T; i += NUM_THREADS) {
+      const int it = b0 + i;
+      Steps<G> st;
+      st.init(a, it / n_tiles, it % n_tiles, g_kv);
+      sm->n[i] = (uint16_t)st.count(a);
+    }
+    __syncthreads();
+    // round-robin simulation of the MMA order -> slot, Q buffer, start and completion order
+    if (threadIdx.x == 0) {
+      uint32_t uses = (uint32_t)sm->uses;
+      int r0 = 0, r1 = 0, r2 = 0;          // pending release key per Q buffer
+      int fin0 = 0, fin1 = 0;              // finish key of each slot's current tile
+      int rend0 = 0, rend1 = 0;            // round at which it finishes
+      int cur0 = -1, cur1 = -1;            // its index
+      int k = 0, e = 0;
+      for (int i = 0; i < T; ++i) {
+        const int n = sm->n[i];
+        if (n == 0) {
+          sm->meta[i] = EMPTY_TILE;
+          continue;
+        }
+        int slot, R;
+        if (k < 2) {
+          slot = k;
+          R = -1;
+        } else {
+          slot = fin0 < fin1 ? 0 : 1;
+          R = slot ? rend1 : rend0;
+          sm->eord[e++] = (uint8_t)(slot ? cur1 : cur0);   // its predecessor completes now
+        }
+        int buf;
+        if (k < NQB) {
+          buf = k;
+        } else {
+          buf = (r0 <= r1 && r0 <= r2) ? 0 : (r1 <= r2 ? 1 : 2);
+        }
+        // op (round r, slot s) has key 2*(r+1)+s; last Q K^T at round R+n-1, last P.V at R+n
+        const int rk = 2 * (R + n) + slot;
+        if (buf == 0) r0 = rk; else if (buf == 1) r1 = rk; else r2 = rk;
+        const int fk = 2 * (R + n + 1) + slot;
+        if (slot) { fin1 = fk; rend1 = R + n; cur1 = i; } else { fin0 = fk; rend0 = R + n; cur0 = i; }
+        sm->meta[i] = (uint8_t)(slot | (buf << 1) | (((uses >> buf) & 1u) << 3));
+        uses ^= 1u << buf;
+        ++k;
+      }
+      if (cur0 >= 0 && cur1 >= 0) {
+        sm->eord[e++] = (uint8_t)(fin0 < fin1 ? cur0 : cur1);
+        sm->eord[e++] = (uint8_t)(fin0 < fin1 ? cur1 : cur0);
+      } else if (cur0 >= 0) {
+        sm->eord[e++] = (uint8_t)cur0;
+      }
+      sm->uses = (int)uses;
+      sm->T = T;
+      sm->Tn = k;
+    }
+    __syncthreads();
+    const int Tn = sm->Tn;
+
+    if (warp >= WARP_EPI) {
+      reg_dealloc<REG_EPILOGUE>();
+      // -------------------------------------------------------------- epilogue warpgroup
+      const int quarter = warp & 3;
+      const int row = quarter * 32 + lane;
+      const uint32_t t_row = tmem + (uint32_t(quarter * 32) << 16);
+      for (int e = 0; e < Tn; ++e) {
+        const int i = sm->eord[e];
+        const int t = sm->meta[i] & 1;
+        const int it = b0 + i;
+        const int bh = it / n_tiles, tile = it % n_tiles;
+        const uint32_t par = (t ? tiles1 : tiles0) & 1;
+        if (t) ++tiles1; else ++tiles0;
+        mbar_wait(st_bar + t, par);
+        const float2 stt = sm->stats[t][row];
+        mbar_arrive(st_free + t);
+        mbar_wait(o_bar + t, par);
+        tc_fence_after();
+        const int n_row = tile * BM + row;
+        const bool store = n_row < a.n_q;
+        uint16_t* orow = a.o + (long long)bh * a.o_stride + (long long)n_row * D;
+#pragma unroll 1
+        for (int c = 0; c < D; c += 16) {
+          uint32_t o[16];
+          tmem_ld16(t_row + 256 + t * D + c, o);
+          tmem_wait_ld();
+          if (c + 16 == D) {
+            tc_fence_before();
+            mbar_arrive(o_free + t);      // O of this slot may be overwritten now
+          }
+          uint32_t pk[8];
 #pragma unroll
-        for (int b = 0; b < C::NBOX; ++b)
-          tma_load_3d_hint(dst + b * (BLK * 128), m, kv_full + s, b * 64, v * BLK, bh, pol);
-      };
-      auto start = [&](int t, int from) {
-        int k = from;
-        while (k < Tn && (sch->meta[k] & 1) != t) ++k;
-        kcur[t] = k < Tn ? k : -1;
-        if (kcur[t] < 0) return;
-        const int it = sch->item[sch->ord[k]];
-        bhs[t] = it / n_tiles;
-        st[t].init(a, bhs[t], it % n_tiles, g_kv);
-        nn[t] = sch->n[sch->ord[k]];
-        jn[t] = 0;
-        uint32_t gm;
-        st[t].next(a, vcur[t], gm);
-        load(&tmap_k, vcur[t], bhs[t]);
-      };
-      start(0, 0);
-      start(1, 0);
-      while (kcur[0] >= 0 || kcur[1] >= 0) {
-        for (int t = 0; t < 2; ++t) {
-          if (kcur[t] < 0) continue;
-          load(&tmap_v, vcur[t], bhs[t]);
-          if (++jn[t] < nn[t]) {
+          for (int q = 0; q < 8; ++q)
+            pk[q] = pack_bf16x2(__uint_as_float(o[2 * q]) * stt.x, __uint_as_float(o[2 * q + 1]) * stt.x);
+          if (store) {
+            uint4* dst = reinterpret_cast<uint4*>(orow + c);
+            dst[0] = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+            dst[1] = make_uint4(pk[4], pk[5], pk[6], pk[7]);
+          }
+        }
+        if (a.lse != nullptr && store) a.lse[(long long)bh * a.n_q + n_row] = stt.y;
+      }
+      reg_alloc<REG_LAUNCH>();
+    } else if (warp >= 8) {
+      reg_dealloc<REG_PRODUCER>();
+      if (warp == WARP_KV) {
+        // -------------------------------------------------------------- KV loader
+        if (lane == 0) {
+          const uint64_t pol = policy_evict_last();
+          int icur[2] = {-1, -1}, jn[2] = {0, 0}, nn[2] = {0, 0}, vcur[2] = {0, 0}, bhs[2] = {0, 0};
+          Steps<G> st[2];
+          auto load = [&](const CUtensorMap* m, int v, int bh) {
+            const int s = kv_idx % C::NST;
+            const uint32_t ph = (kv_idx / C::NST) & 1;
+            ++kv_idx;
+            mbar_wait(kv_empty + s, ph ^ 1);
+            uint8_t* dst = sKV + s * C::STAGE_BYTES;
+            mbar_arrive_expect_tx(kv_full + s, C::STAGE_BYTES);
+#pragma unroll
+            for (int b = 0; b < C::NBOX; ++b)
+              tma_load_3d_hint(dst + b * (BLK * 128), m, kv_full + s, b * 64, v * BLK, bh, pol);
+          };
+          auto start = [&](int t, int from) {
+            int i = from;
+            while (i < T && (sm->meta[i] == EMPTY_TILE || (sm->meta[i] & 1) != t)) ++i;
+            icur[t] = i < T ? i : -1;
+            if (icur[t] < 0) return;
+            const int it = b0 + i;
+            bhs[t] = it / n_tiles;
+            st[t].init(a, bhs[t], it % n_tiles, g_kv);
+            nn[t] = sm->n[i];
+            jn[t] = 0;
             uint32_t gm;
             st[t].next(a, vcur[t], gm);
             load(&tmap_k, vcur[t], bhs[t]);
-          } else {
-            start(t, kcur[t] + 1);
+          };
+          start(0, 0);
+          start(1, 0);
+          while (icur[0] >= 0 || icur[1] >= 0) {
+            for (int t = 0; t < 2; ++t) {
+              if (icur[t] < 0) continue;
+              load(&tmap_v, vcur[t], bhs[t]);
+              if (++jn[t] < nn[t]) {
+                uint32_t gm;
+                st[t].next(a, vcur[t], gm);
+                load(&tmap_k, vcur[t], bhs[t]);
+              } else {
+                start(t, icur[t] + 1);
+              }
+            }
           }
         }
-      }
-    }
-  } else if (warp == WARP_Q) {
-    // ---------------------------------------------------------------- Q loader (start order)
-    if (lane == 0) {
-      for (int k = 0; k < Tn; ++k) {
-        const int meta = sch->meta[k];
-        const int buf = (meta >> 1) & 3;
-        const uint32_t use_par = (meta >> 3) & 1;
-        if (k >= NQB) mbar_wait(q_empty + buf, use_par ^ 1);
-        const int it = sch->item[sch->ord[k]];
-        uint8_t* dst = sQ + buf * C::Q_BYTES;
-        mbar_arrive_expect_tx(q_full + buf, C::Q_BYTES);
+      } else if (warp == WARP_Q) {
+        // -------------------------------------------------------------- Q loader (start order)
+        if (lane == 0) {
+          for (int i = 0; i < T; ++i) {
+            const int meta = sm->meta[i];
+            if (meta == EMPTY_TILE) continue;
+            const int buf = (meta >> 1) & 3;
+            const uint32_t use_par = (meta >> 3) & 1;
+            if (q_used & (1u << buf)) mbar_wait(q_empty + buf, use_par ^ 1);
+            q_used |= 1u << buf;
+            const int it = b0 + i;
+            uint8_t* dst = sQ + buf * C::Q_BYTES;
+            mbar_arrive_expect_tx(q_full + buf, C::Q_BYTES);
 #pragma unroll
-        for (int b = 0; b < C::NBOX; ++b)
-          tma_load_3d(dst + b * (BM * 128), &tmap_q, q_full + buf, b * 64, (it % n_tiles) * BM,
-                      it / n_tiles);
-      }
-    }
-    // empty tiles (no listed block in any of their query blocks): zero output, lse = -inf
-    for (int i = 0; i < sch->T; ++i) {
-      if (sch->n[i] != 0) continue;
-      const int it = sch->item[i];
-      const int bh = it / n_tiles, tile = it % n_tiles;
-      for (int r = lane; r < BM; r += 32) {
-        const int row = tile * BM + r;
-        if (row >= a.n_q) continue;
-        uint4* dst = reinterpret_cast<uint4*>(a.o + (long long)bh * a.o_stride + (long long)row * D);
-        for (int c = 0; c < D / 8; ++c) dst[c] = make_uint4(0, 0, 0, 0);
-        if (a.lse != nullptr) a.lse[(long long)bh * a.n_q + row] = -INFINITY;
-      }
-    }
-  } else if (warp == WARP_MMA) {
-    // ---------------------------------------------------------------- tcgen05 issuer
-    // The whole warp runs the control flow so descriptors stay warp-uniform (uniform registers,
-    // no per-instruction ELECT/R2UR loops); one elected lane issues each tcgen05 instruction.
-    constexpr uint32_t IDESC_QK = idesc_bf16_f32(BM, BLK, 0, 0);
-    constexpr uint32_t IDESC_PV = idesc_bf16_f32(BM, D, 0, 1);
-    const bool leader = elect_one();
-    const uint32_t kv_base = smem_u32(sKV);
-    const uint32_t q_base0 = smem_u32(sQ);
-    // descriptor "lo" words advance by (bytes >> 4); the hi word is constant per operand kind
-    const uint64_t dq0 = sdesc_sw128(q_base0, 16, 1024);
-    const uint64_t dk0 = sdesc_sw128(kv_base, 16, 1024);
-    const uint64_t dv0 = sdesc_sw128(kv_base, BLK * 128, 1024);
-    int kcur[2] = {-1, -1}, jn[2] = {0, 0}, nn[2] = {0, 0}, qb[2] = {0, 0};
-    uint32_t p_cnt[2] = {0, 0};
-    int idx = 0;
-    auto next_stage = [&]() -> uint32_t {
-      const int s = idx % C::NST;
-      const uint32_t ph = (idx / C::NST) & 1;
-      ++idx;
-      mbar_wait(kv_full + s, ph);
-      tc_fence_after();
-      return (uint32_t)s;
-    };
-    auto issue_qk = [&](int t) {
-      const uint32_t s = next_stage();
-      const uint64_t da = dq0 + ((uint64_t)(qb[t] * C::Q_BYTES) >> 4);
-      const uint64_t db = dk0 + ((uint64_t)(s * C::STAGE_BYTES) >> 4);
-      const uint32_t d_tmem = tmem + t * 128;
-      if (leader) {
-#pragma unroll
-        for (int kk = 0; kk < D / 16; ++kk) {
-          const uint32_t oa = ((kk >> 2) * (BM * 128) + (kk & 3) * 32) >> 4;
-          const uint32_t ob = ((kk >> 2) * (BLK * 128) + (kk & 3) * 32) >> 4;
-          mma_ss(d_tmem, da + oa, db + ob, IDESC_QK, kk > 0);
+            for (int b = 0; b < C::NBOX; ++b)
+              tma_load_3d(dst + b * (BM * 128), &tmap_q, q_full + buf, b * 64,
+                          (it % n_tiles) * BM, it / n_tiles);
+          }
         }
-        mma_commit(kv_empty + s);
-        mma_commit(s_bar + t);
-        if (jn[t] == nn[t] - 1) mma_commit(q_empty + qb[t]);   // last use of this Q buffer
-      }
-      __syncwarp();
-    };
-    auto start = [&](int t, int from) {
-      int k = from;
-      while (k < Tn && (sch->meta[k] & 1) != t) ++k;
-      kcur[t] = k < Tn ? k : -1;
-      if (kcur[t] < 0) return;
-      const int meta = sch->meta[k];
-      qb[t] = (meta >> 1) & 3;
-      nn[t] = sch->n[sch->ord[k]];
-      jn[t] = 0;
-      mbar_wait(q_full + qb[t], (meta >> 3) & 1);
-      tc_fence_after();
-      issue_qk(t);
-    };
-    start(0, 0);
-    start(1, 0);
-    while (kcur[0] >= 0 || kcur[1] >= 0) {
-#pragma unroll
-      for (int t = 0; t < 2; ++t) {
-        if (kcur[t] < 0) continue;
-        mbar_wait(p_bar + t, p_cnt[t] & 1);
-        ++p_cnt[t];
-        tc_fence_after();
-        {  // O_t += P_t V_j
-          const uint32_t s = next_stage();
-          const uint64_t dv = dv0 + ((uint64_t)(s * C::STAGE_BYTES) >> 4);
-          const uint32_t o_tmem = tmem + 256 + t * D;
-          const uint32_t p_tmem = tmem + t * 128;
+      } else if (warp == WARP_ZERO) {
+        // -------------------------------------------------------------- empty tiles
+        // no listed block in any of the tile's query blocks: zero output, lse = -inf
+        for (int i = 0; i < T; ++i) {
+          if (sm->meta[i] != EMPTY_TILE) continue;
+          const int it = b0 + i;
+          const int bh = it / n_tiles, tile = it % n_tiles;
+          for (int r = lane; r < BM; r += 32) {
+            const int row = tile * BM + r;
+            if (row >= a.n_q) continue;
+            uint4* dst =
+                reinterpret_cast<uint4*>(a.o + (long long)bh * a.o_stride + (long long)row * D);
+            for (int c = 0; c < D / 8; ++c) dst[c] = make_uint4(0, 0, 0, 0);
+            if (a.lse != nullptr) a.lse[(long long)bh * a.n_q + row] = -INFINITY;
+          }
+        }
+      } else if (warp == WARP_MMA) {
+        // -------------------------------------------------------------- tcgen05 issuer
+        // The whole warp runs the control flow so descriptors stay warp-uniform (uniform
+        // registers); one elected lane issues each tcgen05 instruction.
+        constexpr uint32_t IDESC_QK = idesc_bf16_f32(BM, BLK, 0, 0);
+        constexpr uint32_t IDESC_PV = idesc_bf16_f32(BM, D, 0, 1);
+        constexpr int KH = BLK >= 64 ? BLK / 32 : BLK / 16;  // P.V K-steps of the first P half
+        const bool leader = elect_one();
+        const uint64_t dq0 = sdesc_sw128(smem_u32(sQ), 16, 1024);
+        const uint64_t dk0 = sdesc_sw128(smem_u32(sKV), 16, 1024);
+        const uint64_t dv0 = sdesc_sw128(smem_u32(sKV), BLK * 128, 1024);
+        int icur0 = -1, icur1 = -1, jn0 = 0, jn1 = 0, nn0 = 0, nn1 = 0, qb0 = 0, qb1 = 0;
+        auto next_stage = [&]() -> uint32_t {
+          const int s = kv_idx % C::NST;
+          const uint32_t ph = (kv_idx / C::NST) & 1;
+          ++kv_idx;
+          mbar_wait(kv_full + s, ph);
+          return (uint32_t)s;
+        };
+        auto issue_qk = [&](int t, uint32_t s, int qb, bool last) {
+          const uint64_t da = dq0 + ((uint64_t)(qb * C::Q_BYTES) >> 4);
+          const uint64_t db = dk0 + ((uint64_t)(s * C::STAGE_BYTES) >> 4);
           if (leader) {
 #pragma unroll
-            for (int kk = 0; kk < BLK / 16; ++kk)
-              mma_ts(o_tmem, p_tmem + kk * 8, dv + ((uint32_t)(kk * 2048) >> 4), IDESC_PV,
-                     (jn[t] > 0 || kk > 0) ? 1u : 0u);
-            mma_commit(kv_empty + s);
-          }
-          __syncwarp();
-        }
-        if (++jn[t] < nn[t]) {
-          issue_qk(t);
-        } else {
-          if (leader) mma_commit(o_bar + t);
-          __syncwarp();
-          start(t, kcur[t] + 1);
-        }
-      }
-    }
-  }
-  } else {
-    // ---------------------------------------------------------------- softmax warpgroups
-    reg_alloc<REG_SOFTMAX>();
-    const int t = warp >> 2;                 // slot
-    const int quarter = warp & 3;
-    const int row = quarter * 32 + lane;
-    const uint32_t t_row = tmem + (uint32_t(quarter * 32) << 16);
-    const uint32_t s_col = t * 128;
-    const uint32_t o_col = 256 + t * D;
-    const int grp = row / BLK;
-    const float sl2 = a.scale_log2;
-    const uint64_t sl2x2 = f2_pack(sl2, sl2);
-    uint32_t s_cnt = 0, o_cnt = 0;
-    for (int k = 0; k < Tn; ++k) {
-      if ((sch->meta[k] & 1) != t) continue;
-      const int it = sch->item[sch->ord[k]];
-      const int bh = it / n_tiles, tile = it % n_tiles;
-      Steps<G> st;
-      st.init(a, bh, tile, g_kv);
-      float m = -INFINITY;   // running max of s * scale * log2(e)
-      float l = 0.f;         // running sum of exp2(s * sl2 - m)
-      int v;
-      uint32_t gm;
-      bool have = st.next(a, v, gm);
-      int j = 0;
-      while (have) {
-        SV_STAMP(0, 5 * s_cnt + 0)
-        mbar_wait(s_bar + t, s_cnt & 1);
-        SV_STAMP(0, 5 * s_cnt + 1)
-        ++s_cnt;
-        tc_fence_after();
-        uint32_t sr[BLK];
-        if constexpr (BLK >= 32) {
-#pragma unroll
-          for (int c = 0; c < BLK; c += 32) tmem_ld32(t_row + s_col + c, sr + c);
-        } else {
-#pragma unroll
-          for (int c = 0; c < BLK; c += 8) tmem_ld8(t_row + s_col + c, sr + c);
-        }
-        // next step's block index: the load's latency hides under this step
-        int v_n;
-        uint32_t gm_n;
-        const bool have_n = st.next(a, v_n, gm_n);
-        tmem_wait_ld();
-        const bool row_on = (gm >> grp) & 1u;
-        const int valid = row_on ? min(BLK, a.n_kv - v * BLK) : 0;
-        // ragged last KV block / rows whose query block does not list this step (warp-uniform
-        // branch, rarely taken)
-        if (__builtin_expect(__any_sync(0xffffffffu, valid < BLK), 0)) {
-#pragma unroll
-          for (int c = 0; c < BLK; ++c)
-            if (c >= valid) sr[c] = __float_as_uint(-INFINITY);
-        }
-        float mx;
-        {
-          float mm[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
-#pragma unroll
-          for (int c = 0; c + 8 <= BLK; c += 8) {
-            const int q = (c >> 3) & 3;
-            mm[q] = fmax3(mm[q], __uint_as_float(sr[c]), __uint_as_float(sr[c + 1]));
-            mm[q] = fmax3(mm[q], __uint_as_float(sr[c + 2]), __uint_as_float(sr[c + 3]));
-            mm[q] = fmax3(mm[q], __uint_as_float(sr[c + 4]), __uint_as_float(sr[c + 5]));
-            mm[q] = fmax3(mm[q], __uint_as_float(sr[c + 6]), __uint_as_float(sr[c + 7]));
-          }
-          mx = fmax3(fmaxf(mm[0], mm[1]), mm[2], mm[3]);
-        }
-        SV_STAMP(0, 5 * (s_cnt - 1) + 2)
-        const float mx_s = mx * sl2;
-        const bool need = mx_s > m + 8.0f;
-        float alpha = 1.f;
-        if (need) {
-          alpha = ex2(m - mx_s);
-          m = mx_s;
-          l *= alpha;
-        }
-        const float mref = (m == -INFINITY) ? 0.f : m;
-        const uint64_t negm = f2_pack(-mref, -mref);
-        uint64_t acc[4] = {0, 0, 0, 0};
-        constexpr int CH = BLK < 32 ? BLK : 32;
-#pragma unroll
-        for (int c0 = 0; c0 < BLK; c0 += CH) {
-          uint32_t p[CH / 2];
-#pragma unroll
-          for (int c = 0; c < CH; c += 2) {
-            const uint64_t x = ffma2(f2_pack(__uint_as_float(sr[c0 + c]), __uint_as_float(sr[c0 + c + 1])),
-                                     sl2x2, negm);
-            float p0, p1;
-            if (EMU_EVERY > 0 && ((c0 + c) / 2) % (EMU_EVERY > 0 ? EMU_EVERY : 1) == EMU_EVERY - 1) {
-              ex2_emu2(x, p0, p1);
-            } else {
-              float x0, x1;
-              f2_unpack(x, x0, x1);
-              p0 = ex2(x0);
-              p1 = ex2(x1);
+            for (int kk = 0; kk < D / 16; ++kk) {
+              const uint32_t oa = ((kk >> 2) * (BM * 128) + (kk & 3) * 32) >> 4;
+              const uint32_t ob = ((kk >> 2) * (BLK * 128) + (kk & 3) * 32) >> 4;
+              mma_ss(tmem + t * 128, da + oa, db + ob, IDESC_QK, kk > 0);
             }
-            acc[(c >> 1) & 3] = fadd2(acc[(c >> 1) & 3], f2_pack(p0, p1));
-            p[c / 2] = pack_bf16x2(p0, p1);
+            mma_commit(kv_empty + s);
+            mma_commit(s_bar + t);
+            if (last) mma_commit(q_empty + qb);   // last use of this Q buffer
           }
-          // P chunk c0 lands in columns [c0/2, c0/2 + CH/2) of S, all already read
-          if constexpr (CH == 32) {
-            tmem_st16(t_row + s_col + c0 / 2, p);
-          } else {
+          __syncwarp();
+        };
+        auto start = [&](int t, int from) {
+          int i = from;
+          while (i < T && (sm->meta[i] == EMPTY_TILE || (sm->meta[i] & 1) != t)) ++i;
+          const int ic = i < T ? i : -1;
+          if (t) icur1 = ic; else icur0 = ic;
+          if (ic < 0) return;
+          const int meta = sm->meta[ic];
+          const int qb = (meta >> 1) & 3;
+          const int n = sm->n[ic];
+          if (t) { qb1 = qb; nn1 = n; jn1 = 0; } else { qb0 = qb; nn0 = n; jn0 = 0; }
+          const uint32_t s = next_stage();
+          mbar_wait(q_full + qb, (meta >> 3) & 1);
+          tc_fence_after();
+          issue_qk(t, s, qb, n == 1);
+        };
+        start(0, 0);
+        start(1, 0);
+        while (icur0 >= 0 || icur1 >= 0) {
 #pragma unroll
-            for (int c = 0; c < CH / 2; c += 8) tmem_st8(t_row + s_col + c0 / 2 + c, p + c);
-          }
-        }
-        {
-          SV_STAMP(0, 5 * (s_cnt - 1) + 3)
-          const uint64_t s2 = fadd2(fadd2(acc[0], acc[1]), fadd2(acc[2], acc[3]));
-          float s0, s1;
-          f2_unpack(s2, s0, s1);
-          l += s0 + s1;
-        }
-        if (j > 0 && __any_sync(0xffffffffu, need)) {
-#pragma unroll 1
-          for (int c = 0; c < D; c += 32) {
-            uint32_t o[32];
-            tmem_ld32(t_row + o_col + c, o);
-            tmem_wait_ld();
+          for (int t = 0; t < 2; ++t) {
+            const int icur = t ? icur1 : icur0;
+            if (icur < 0) continue;
+            const int jn = t ? jn1 : jn0, nn = t ? nn1 : nn0, qb = t ? qb1 : qb0;
+            const int tdone = t ? tiles1 : tiles0;
+            // the stages this op reads are (normally) resident already: check them before P
+            const uint32_t sv = next_stage();
+            const bool more = jn + 1 < nn;
+            const uint32_t sk = more ? next_stage() : 0u;
+            const uint32_t par = (t ? p_cnt1 : p_cnt0) & 1;
+            if (t) ++p_cnt1; else ++p_cnt0;
+            const uint64_t dv = dv0 + ((uint64_t)(sv * C::STAGE_BYTES) >> 4);
+            const uint32_t o_tmem = tmem + 256 + t * D;
+            const uint32_t p_tmem = tmem + t * 128;
+            // the tile's first P.V overwrites O: the epilogue must have drained the previous one
+            if (jn == 0 && tdone > 0) mbar_wait(o_free + t, (tdone - 1) & 1);
+            // O_t += P_t V_j in two halves: the first as soon as half of P is in TMEM
+            mbar_wait(p_bar + 2 * t, par);
+            tc_fence_after();
+            if (leader) {
 #pragma unroll
-            for (int i = 0; i < 32; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * alpha);
-            tmem_st32(t_row + o_col + c, o);
+              for (int kk = 0; kk < KH; ++kk)
+                mma_ts(o_tmem, p_tmem + kk * 8, dv + ((uint32_t)(kk * 2048) >> 4), IDESC_PV,
+                       (jn > 0 || kk > 0) ? 1u : 0u);
+            }
+            __syncwarp();
+            mbar_wait(p_bar + 2 * t + 1, par);
+            tc_fence_after();
+            if (leader) {
+#pragma unroll
+              for (int kk = KH; kk < BLK / 16; ++kk)
+                mma_ts(o_tmem, p_tmem + kk * 8, dv + ((uint32_t)(kk * 2048) >> 4), IDESC_PV, 1u);
+              mma_commit(kv_empty + sv);
+            }
+            __syncwarp();
+            if (more) {
+              if (t) ++jn1; else ++jn0;
+              issue_qk(t, sk, qb, jn + 2 == nn);
+            } else {
+              if (leader) mma_commit(o_bar + t);
+              __syncwarp();
+              if (t) ++tiles1; else ++tiles0;
+              start(t, icur + 1);
+            }
           }
         }
-        tmem_wait_st();
-        tc_fence_before();
-        mbar_arrive(p_bar + t);
-        SV_STAMP(0, 5 * (s_cnt - 1) + 4)
-        ++j;
-        v = v_n;
-        gm = gm_n;
-        have = have_n;
       }
-      // ------------------------------------------------------------ epilogue of this tile
-      mbar_wait(o_bar + t, o_cnt & 1);
-      ++o_cnt;
-      tc_fence_after();
-      const int n_row = tile * BM + row;
-      const bool store = n_row < a.n_q;
-      const bool live = m != -INFINITY;        // the row saw at least one valid logit
-      const float inv = live ? 1.f / l : 0.f;
-      uint16_t* orow = a.o + (long long)bh * a.o_stride + (long long)n_row * D;
+      reg_alloc<REG_LAUNCH>();
+    } else {
+      // ---------------------------------------------------------------- softmax warpgroups
+      reg_alloc<REG_SOFTMAX>();
+      const int t = warp >> 2;                 // slot
+      const int quarter = warp & 3;
+      const int row = quarter * 32 + lane;
+      const uint32_t t_row = tmem + (uint32_t(quarter * 32) << 16);
+      const uint32_t s_col = t * 128;
+      const uint32_t o_col = 256 + t * D;
+      const int grp = row / BLK;
+      const float sl2 = a.scale_log2;
+      const uint64_t sl2x2 = f2_pack(sl2, sl2);
+      for (int i = 0; i < T; ++i) {
+        const int meta = sm->meta[i];
+        if (meta == EMPTY_TILE || (meta & 1) != t) continue;
+        const int it = b0 + i;
+        Steps<G> st;
+        st.init(a, it / n_tiles, it % n_tiles, g_kv);
+        float m = -INFINITY;   // running max of s * scale * log2(e)
+        float l = 0.f;         // running sum of exp2(s * sl2 - m)
+        int v;
+        uint32_t gm;
+        bool have = st.next(a, v, gm);
+        int j = 0;
+        while (have) {
+          SV_STAMP(5 * s_cnt + 0)
+          mbar_wait(s_bar + t, s_cnt & 1);
+          SV_STAMP(5 * s_cnt + 1)
+          ++s_cnt;
+          tc_fence_after();
+          uint32_t sr[BLK];
+          // next step's block index: the load's latency hides under this step
+          int v_n;
+          uint32_t gm_n;
+          bool have_n;
+          const bool row_on = (gm >> grp) & 1u;
+          const int valid = row_on ? min(BLK, a.n_kv - v * BLK) : 0;
+          float mx;
+          {
+            float mm[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+            auto mask_and_max = [&](int c_lo, int c_hi) {
+              // ragged last KV block / rows whose query block does not list this step
+              // (warp-uniform branch, rarely taken)
+              if (__builtin_expect(__any_sync(0xffffffffu, valid < c_hi), 0)) {
+#pragma unroll
+                for (int c = 0; c < BLK; ++c)
+                  if (c >= c_lo && c < c_hi && c >= valid) sr[c] = __float_as_uint(-INFINITY);
+              }
+#pragma unroll
+              for (int c = 0; c + 8 <= BLK; c += 8) {
+                if (c < c_lo || c >= c_hi) continue;
+                const int q = (c >> 3) & 3;
+                mm[q] = fmax3(mm[q], __uint_as_float(sr[c]), __uint_as_float(sr[c + 1]));
+                mm[q] = fmax3(mm[q], __uint_as_float(sr[c + 2]), __uint_as_float(sr[c + 3]));
+                mm[q] = fmax3(mm[q], __uint_as_float(sr[c + 4]), __uint_as_float(sr[c + 5]));
+                mm[q] = fmax3(mm[q], __uint_as_float(sr[c + 6]), __uint_as_float(sr[c + 7]));
+              }
+            };
+            if constexpr (BLK >= 64) {
+              // two halves: the second half's TMEM load overlaps the first half's max
+#pragma unroll
+              for (int c = 0; c < BLK / 2; c += 32) tmem_ld32(t_row + s_col + c, sr + c);
+              tmem_wait_ld();
+#pragma unroll
+              for (int c = BLK / 2; c < BLK; c += 32) tmem_ld32(t_row + s_col + c, sr + c);
+              have_n = st.next(a, v_n, gm_n);
+              mask_and_max(0, BLK / 2);
+              tmem_wait_ld();
+              mask_and_max(BLK / 2, BLK);
+            } else {
+              if constexpr (BLK == 32) {
+                tmem_ld32(t_row + s_col, sr);
+              } else {
+#pragma unroll
+                for (int c = 0; c < BLK; c += 8) tmem_ld8(t_row + s_col + c, sr + c);
+              }
+              have_n = st.next(a, v_n, gm_n);
+              tmem_wait_ld();
+              mask_and_max(0, BLK);
+            }
+            mx = fmax3(fmaxf(mm[0], mm[1]), mm[2], mm[3]);
+          }
+          SV_STAMP(5 * (s_cnt - 1) + 2)
+          const float mx_s = mx * sl2;
+          const bool need = mx_s > m + 8.0f;
+          float alpha = 1.f;
+          if (need) {
+            alpha = ex2(m - mx_s);
+            m = mx_s;
+            l *= alpha;
+          }
+          // lazy rescale of O (rare): P_{j-1} V_{j-1} is complete (covered by the S_j commit) and
+          // P_j V_j is not issued before this thread arrives on p_bar
+          if (j > 0 && __any_sync(0xffffffffu, need)) {
 #pragma unroll 1
-      for (int c = 0; c < D; c += 32) {
-        uint32_t o[32];
-        tmem_ld32(t_row + o_col + c, o);
-        tmem_wait_ld();
-        uint32_t pk[16];
+            for (int c = 0; c < D; c += 32) {
+              uint32_t o[32];
+              tmem_ld32(t_row + o_col + c, o);
+              tmem_wait_ld();
 #pragma unroll
-        for (int i = 0; i < 16; ++i)
-          pk[i] = pack_bf16x2(__uint_as_float(o[2 * i]) * inv, __uint_as_float(o[2 * i + 1]) * inv);
-        if (store) {
-          uint4* dst = reinterpret_cast<uint4*>(orow + c);
+              for (int i = 0; i < 32; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * alpha);
+              tmem_st32(t_row + o_col + c, o);
+            }
+          }
+          const float mref = (m == -INFINITY) ? 0.f : m;
+          const uint64_t negm = f2_pack(-mref, -mref);
+          uint64_t acc[4] = {0, 0, 0, 0};
+          constexpr int CH = BLK < 32 ? BLK : 32;
 #pragma unroll
-          for (int i = 0; i < 4; ++i)
-            dst[i] = make_uint4(pk[4 * i], pk[4 * i + 1], pk[4 * i + 2], pk[4 * i + 3]);
+          for (int c0 = 0; c0 < BLK; c0 += CH) {
+            uint32_t p[CH / 2];
+#pragma unroll
+            for (int c = 0; c < CH; c += 2) {
+              const uint64_t x = ffma2(f2_pack(__uint_as_float(sr[c0 + c]), __uint_as_float(sr[c0 + c + 1])),
+                                       sl2x2, negm);
+              float p0, p1;
+              if (EMU_EVERY > 0 && ((c0 + c) / 2) % (EMU_EVERY > 0 ? EMU_EVERY : 1) == EMU_EVERY - 1) {
+                ex2_emu2(x, p0, p1);
+              } else {
+                float x0, x1;
+                f2_unpack(x, x0, x1);
+                p0 = ex2(x0);
+                p1 = ex2(x1);
+              }
+              acc[(c >> 1) & 3] = fadd2(acc[(c >> 1) & 3], f2_pack(p0, p1));
+              p[c / 2] = pack_bf16x2(p0, p1);
+            }
+            // P chunk c0 lands in columns [c0/2, c0/2 + CH/2) of S, all already read
+            if constexpr (CH == 32) {
+              tmem_st16(t_row + s_col + c0 / 2, p);
+            } else {
+#pragma unroll
+              for (int c = 0; c < CH / 2; c += 8) tmem_st8(t_row + s_col + c0 / 2 + c, p + c);
+            }
+            if (BLK >= 64 && c0 + CH == BLK / 2) {
+              // first half of P is in TMEM: let the MMA warp start P.V on it
+              tmem_wait_st();
+              tc_fence_before();
+              mbar_arrive(p_bar + 2 * t);
+            }
+          }
+          {
+            SV_STAMP(5 * (s_cnt - 1) + 3)
+            const uint64_t s2 = fadd2(fadd2(acc[0], acc[1]), fadd2(acc[2], acc[3]));
+            float s0, s1;
+            f2_unpack(s2, s0, s1);
+            l += s0 + s1;
+          }
+          tmem_wait_st();
+          tc_fence_before();
+          if (BLK < 64) mbar_arrive(p_bar + 2 * t);
+          mbar_arrive(p_bar + 2 * t + 1);
+          SV_STAMP(5 * (s_cnt - 1) + 4)
+          ++j;
+          v = v_n;
+          gm = gm_n;
+          have = have_n;
         }
+        // hand the row statistics to the epilogue warpgroup
+        const int tdone = t ? tiles1 : tiles0;
+        if (tdone > 0) mbar_wait(st_free + t, (tdone - 1) & 1);
+        if (t) ++tiles1; else ++tiles0;
+        const bool live = m != -INFINITY;      // the row saw at least one valid logit
+        sm->stats[t][row] = make_float2(live ? 1.f / l : 0.f,
+                                        live ? (m * 0.69314718055994531f + logf(l)) : -INFINITY);
+        mbar_arrive(st_bar + t);
       }
-      if (a.lse != nullptr && store)
-        a.lse[(long long)bh * a.n_q + n_row] =
-            live ? (m * 0.69314718055994531f + logf(l)) : -INFINITY;
-      tc_fence_before();
+      reg_dealloc<REG_LAUNCH>();
     }
+    __syncthreads();
   }
 
   tc_fence_before();
@@ -713,17 +848,13 @@ cudaError_t launch_t(const CUtensorMap& tq, const CUtensorMap& tk, const CUtenso
   if (e != cudaSuccess) return e;
   const int n_tiles = (a.n_q + BM - 1) / BM;
   const long long items = (long long)n_tiles * a.bh;
+  if (items <= 0) return cudaSuccess;
+  if (items > (1LL << 30)) return cudaErrorInvalidValue;
   const int sms = num_sms();
-  for (long long b0 = 0; b0 < items; b0 += (long long)sms * MAX_TILES) {
-    const long long b1 = b0 + (long long)sms * MAX_TILES < items ? b0 + (long long)sms * MAX_TILES : items;
-    const long long cnt = b1 - b0;
-    // two tile slots per CTA: fewer CTAs than SMs when there is little work
-    const int grid = (int)(cnt >= 2LL * sms ? sms : (cnt + 1) / 2);
-    kern<<<grid, NUM_THREADS, C::SMEM, st>>>(tq, tk, tv, a, (int)b0, (int)b1);
-    e = cudaGetLastError();
-    if (e != cudaSuccess) return e;
-  }
-  return cudaSuccess;
+  // two tile slots per CTA: fewer CTAs than SMs when there is little work
+  const int grid = (int)(items >= 2LL * sms ? sms : (items + 1) / 2);
+  kern<<<grid, NUM_THREADS, C::SMEM, st>>>(tq, tk, tv, a, 0, (int)items);
+  return cudaGetLastError();
 }
 
 }  // namespace

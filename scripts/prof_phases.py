@@ -38,13 +38,9 @@ print("median clk: wait %.0f  pass1(max) %.0f  pass2(exp) %.0f  tail %.0f  gap->
 print("first 12 steps (wait, pass1, pass2, tail):")
 print(d[:12])
 
-mm = a[4096:4096 + 6 * 682].reshape(-1, 6)
-mm = mm[(mm[:, 0] > 0) & (mm[:, 5] > 0)]
-if len(mm):
-    dm = np.diff(mm, axis=1)
-    print("MMA slot0 median clk: p_wait %.0f  V_ready %.0f  PV_issue %.0f  K_ready %.0f  QK_issue %.0f" %
-          tuple(np.median(dm, axis=0)))
-    print(dm[:8])
-
-pv = a[4096 + 4010:4096 + 4018]; qk = a[4096 + 4000:4096 + 4008]
-print("per-MMA issue deltas PV:", np.diff(pv), " QK:", np.diff(qk))
+st0 = a[7400:7400 + 148]; su = a[7600:7600 + 148]; en = a[7800:7800 + 148]
+if st0.min() > 0:
+    t0 = st0.min()
+    print("CTA start spread us: %.2f   setup (median) us: %.2f   end: min %.2f median %.2f max %.2f us" % (
+        (st0.max() - t0) / 1e3, np.median(su - st0) / 1e3, (en.min() - t0) / 1e3, np.median(en - t0) / 1e3,
+        (en.max() - t0) / 1e3))
