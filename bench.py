@@ -43,7 +43,7 @@ K_T, S_D, BLOCK, D, SINK, WINDOWS, TOPK = 13, 11, 128, 128, 5, (7, 5, 3, 1, 1), 
 def parse():
     p = argparse.ArgumentParser()
     p.add_argument("--gpus", type=int, default=1)
-    p.add_argument("--steps", type=int, default=20)
+    p.add_argument("--steps", type=int, default=50)
     p.add_argument("--warmup", type=int, default=5)
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
     p.add_argument("--config", default="8b", choices=list(CONFIGS))
