@@ -232,9 +232,11 @@ class SparseLayer:
 
     def __init__(self, sides, target: int, decision: int, block: int, bh: int,
                  sink_scales: int = 5, windows=(7, 5, 3, 1, 1), select_mode=SELECT_TOPK,
-                 topk: int = 5, threshold: float = 0.01, map_mode=MAP_FOOTPRINT):
+                 topk: int = 5, threshold: float = 0.01, map_mode=MAP_FOOTPRINT,
+                 kinds: Sequence[str] = ("csla", "cs4a", "union")):
         self.sides, self.K, self.S, self.B, self.bh = list(sides), target, decision, block, bh
         self.sink, self.windows = sink_scales, tuple(windows)
+        self.kinds = tuple(kinds)   # list sets built by build_patterns (READING 19 policies)
         self.select_mode, self.topk, self.threshold, self.map_mode = select_mode, topk, threshold, map_mode
         gk, gs = geometry(sides, target, block), geometry(sides, decision, block)
         self.gk, self.gs = gk, gs
@@ -245,7 +247,7 @@ class SparseLayer:
         self.mapped = torch.empty((bh, gk["G_q"], gk["W"]), dtype=torch.int32, device=dev)
         cap = bh * gk["G_q"] * gk["G_kv"]
         self.lists = {}
-        for name in ("csla", "cs4a", "union"):
+        for name in self.kinds:
             self.lists[name] = (torch.empty(bh * gk["G_q"] + 1, dtype=torch.int32, device=dev),
                                 torch.empty(cap, dtype=torch.int32, device=dev))
         self.status = torch.zeros(1, dtype=torch.int32, device=dev)
@@ -260,11 +262,14 @@ class SparseLayer:
         map_indices(self.sides, self.S, self.K, self.B, self.sink, self.src, self.map_mode,
                     out=self.mapped, stream=stream)
         g = self.gk
-        for name, masks in (("csla", [(self.local, True)]), ("cs4a", [(self.mapped, False)]),
-                            ("union", [(self.local, True), (self.mapped, False)])):
+        for name in self.kinds:
             rp, ci = self.lists[name]
-            build_block_lists(self.bh, g["G_q"], g["G_kv"], masks, self.cap, rp, ci, self.status,
-                              stream=stream)
+            build_block_lists(self.bh, g["G_q"], g["G_kv"], self._masks(name), self.cap, rp, ci,
+                              self.status, stream=stream)
+
+    def _masks(self, which):
+        return {"csla": [(self.local, True)], "cs4a": [(self.mapped, False)],
+                "union": [(self.local, True), (self.mapped, False)]}[which]
 
     def attend(self, which: str, q, k_cache, v_cache, o=None, lse=None, stream=None):
         """a6 on the lists `which` in {'csla', 'cs4a', 'union'}."""

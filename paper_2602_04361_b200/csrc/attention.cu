@@ -32,6 +32,7 @@
 
 #include "kernels.h"
 #include "ptx.cuh"
+#include "kernel_util.cuh"
 
 #ifdef SV_PROF
 // Development instrumentation (variant libraries only, scripts/build_variant.sh).
@@ -163,73 +164,6 @@ struct Steps {
     return n;
   }
 };
-
-__device__ __forceinline__ bool elect_one() {
-  uint32_t pred;
-  asm volatile(
-      "{\n\t.reg .pred p;\n\t"
-      "elect.sync _|p, 0xffffffff;\n\t"
-      "selp.u32 %0, 1, 0, p;\n\t}"
-      : "=r"(pred));
-  return pred != 0;
-}
-__device__ __forceinline__ float fmax3(float a, float b, float c) {
-  float d;
-  asm("max.f32 %0, %1, %2, %3;" : "=f"(d) : "f"(a), "f"(b), "f"(c));
-  return d;
-}
-__device__ __forceinline__ uint64_t f2_pack(float lo, float hi) {
-  uint64_t r;
-  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
-  return r;
-}
-__device__ __forceinline__ void f2_unpack(uint64_t r, float& lo, float& hi) {
-  asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(r));
-}
-__device__ __forceinline__ uint64_t ffma2(uint64_t a, uint64_t b, uint64_t c) {
-  uint64_t d;
-  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
-  return d;
-}
-__device__ __forceinline__ uint64_t fadd2(uint64_t a, uint64_t b) {
-  uint64_t d;
-  asm("add.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
-  return d;
-}
-
-template <int N>
-__device__ __forceinline__ void reg_alloc() {
-  asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(N));
-}
-template <int N>
-__device__ __forceinline__ void reg_dealloc() {
-  asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(N));
-}
-
-// 2^x for a pair on the FMA/ALU pipes (offloads MUFU): x = n + f, n = rint(x) via the 1.5*2^23
-// magic add, f in [-1/2, 1/2], 2^f by a degree-3 polynomial (max rel. error 7.5e-5, far below
-// the bf16 rounding P gets), 2^n added to the exponent field.  x is clamped at -126 so masked
-// (-inf) logits give 2^-126 instead of 0: negligible against l >= 1, and rows that never see a
-// valid logit are zeroed by the epilogue (m stays -inf).
-__device__ __forceinline__ void ex2_emu2(uint64_t x2, float& p0, float& p1) {
-  constexpr float MAGIC = 12582912.0f;   // 1.5 * 2^23
-  float x0, x1;
-  f2_unpack(x2, x0, x1);
-  x0 = fmaxf(x0, -126.f);
-  x1 = fmaxf(x1, -126.f);
-  const uint64_t xc = f2_pack(x0, x1);
-  const uint64_t t = fadd2(xc, f2_pack(MAGIC, MAGIC));
-  const uint64_t r = fadd2(t, f2_pack(-MAGIC, -MAGIC));
-  const uint64_t f = ffma2(r, f2_pack(-1.f, -1.f), xc);   // x - rint(x)
-  uint64_t q = ffma2(f2_pack(0.05517166f, 0.05517166f), f, f2_pack(0.24261113f, 0.24261113f));
-  q = ffma2(q, f, f2_pack(0.69326097f, 0.69326097f));
-  q = ffma2(q, f, f2_pack(0.99992806f, 0.99992806f));
-  float q0, q1, t0, t1;
-  f2_unpack(q, q0, q1);
-  f2_unpack(t, t0, t1);
-  p0 = __int_as_float(__float_as_int(q0) + (__float_as_int(t0) << 23));
-  p1 = __int_as_float(__float_as_int(q1) + (__float_as_int(t1) << 23));
-}
 
 // Cost prefix F(i) of the first i items of [item_begin, item_end) (monotone in i): listed blocks
 // (row_ptr prefix sums) + TILE_OVERHEAD per tile.
@@ -765,7 +699,7 @@ attn_fwd_kernel(const __grid_constant__ CUtensorMap tmap_q,
                                        sl2x2, negm);
               float p0, p1;
               if (EMU_EVERY > 0 && ((c0 + c) / 2) % (EMU_EVERY > 0 ? EMU_EVERY : 1) == EMU_EVERY - 1) {
-                ex2_emu2(x, p0, p1);
+                ex2_emu2<3>(x, p0, p1);
               } else {
                 float x0, x1;
                 f2_unpack(x, x0, x1);

@@ -102,18 +102,74 @@ __device__ void mark_image(const Geo& g, int j, int shift, int mode, int B, uint
   }
 }
 
-__global__ void __launch_bounds__(256) map_table_kernel(const Geo g, int S, int K, int B,
+__device__ __forceinline__ uint32_t range_word(int b0, int b1, int w) {
+  const int lo = max(b0, w * 32), hi = min(b1, w * 32 + 31);
+  if (lo > hi) return 0u;
+  const int len = hi - lo + 1;
+  return (len == 32 ? 0xffffffffu : ((1u << len) - 1u)) << (lo - w * 32);
+}
+
+// Image of source block v in the target bit row: OR over v's real tokens (see mark_image).
+// MW > 0: one warp per source block, each lane ORs its tokens' footprint into MW register words,
+// then a warp OR-reduction (no atomics).  MW == 0: shared-memory atomics (wide rows).
+template <int MW>
+__device__ void build_block_image(const Geo& g, int v, int S, int K, int B, int mode, int W_K,
+                                  uint32_t* trow, int lane) {
+  const int n_kvS = g.cum[S];
+  const int shift = K - S;
+  uint32_t acc[MW > 0 ? MW : 1];
+#pragma unroll
+  for (int w = 0; w < (MW > 0 ? MW : 1); ++w) acc[w] = 0u;
+  for (int j = v * B + lane; j < min((v + 1) * B, n_kvS); j += 32) {
+    if constexpr (MW == 0) {
+      mark_image(g, j, shift, mode, B, trow);
+    } else {
+      int l = 1;
+      while (g.cum[l] <= j) ++l;                             // C_{l-1} <= j < C_l
+      const int delta = j - g.cum[l - 1];
+      const int lp = l + shift;
+      const int s = g.side[l - 1], sp = g.side[lp - 1];
+      const int x = delta / s, y = delta % s;
+      const int base = g.cum[lp - 1];
+      int x0, x1, y0, y1;
+      if (mode == 1) {                                       // POINT
+        x0 = x1 = x * sp / s;
+        y0 = y1 = y * sp / s;
+      } else {                                               // FOOTPRINT (READING 14)
+        x0 = x * sp / s; x1 = (x + 1) * sp / s - 1;
+        y0 = y * sp / s; y1 = (y + 1) * sp / s - 1;
+      }
+      for (int xp = x0; xp <= x1; ++xp) {
+        const int b0 = (base + xp * sp + y0) / B, b1 = (base + xp * sp + y1) / B;
+#pragma unroll
+        for (int w = 0; w < MW; ++w) acc[w] |= range_word(b0, b1, w);
+      }
+    }
+  }
+  if constexpr (MW > 0) {
+#pragma unroll
+    for (int w = 0; w < MW; ++w) {
+      const uint32_t r = __reduce_or_sync(0xffffffffu, acc[w]);
+      if (lane == 0 && w < W_K) trow[w] = r;
+    }
+  }
+}
+
+template <int MW>
+__global__ void __launch_bounds__(1024) map_table_kernel(const Geo g, int S, int K, int B,
                                                         int sink_scales, int mode, int G_S,
                                                         int G_K, int G_kvS, int W_S, int W_K,
                                                         int bh_total, int bh_per_cta,
                                                         const uint32_t* __restrict__ src,
                                                         uint32_t* __restrict__ dst) {
   extern __shared__ uint32_t table[];                      // [G_kvS][W_K]
-  const int n_kvS = g.cum[S];
-  for (int i = threadIdx.x; i < G_kvS * W_K; i += blockDim.x) table[i] = 0;
-  __syncthreads();
-  for (int j = threadIdx.x; j < n_kvS; j += blockDim.x)
-    mark_image(g, j, K - S, mode, B, table + (j / B) * W_K);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  if (MW == 0) {
+    for (int i = threadIdx.x; i < G_kvS * W_K; i += blockDim.x) table[i] = 0;
+    __syncthreads();
+  }
+  for (int v = warp; v < G_kvS; v += nw)
+    build_block_image<MW>(g, v, S, K, B, mode, W_K, table + v * W_K, lane);
   __syncthreads();
   // sink blocks v < ceil(C_sink / B) (READING 13)
   const int n_sb = sink_scales > 0 ? (g.cum[sink_scales] + B - 1) / B : 0;
@@ -175,11 +231,15 @@ __global__ void map_kernel(const Geo g, int S, int K, int B, int sink_scales, in
 }
 
 // ------------------------------------------------------------------------------------ a5
-// Single CTA of 1024 threads, one THREAD per row (rows are a few words wide), rows processed in
-// chunks of 1024 with a running carry.  Pass 1: OR the masks' words, popcount, block-wide
-// exclusive scan -> row_ptr.  Pass 2: every thread re-reads its row's words (L1/L2 hits) and
-// writes its set bits in ascending order at row_ptr[r].  All loads of a chunk are in flight at
-// once, so the kernel costs a few memory latencies per chunk.
+// Up to 32 CTAs, each owning a contiguous range of rows.  A CTA first counts the set bits of all
+// rows before its range (coalesced over words; at most a few thousand L2 hits) to get its base
+// offset — no inter-CTA communication, deterministic.  Then, in chunks of blockDim rows: one
+// thread per row ORs the masks' words and counts, a block scan gives row_ptr, and one WARP per
+// row writes the ascending list (ballot prefix per word, coalesced stores).
+constexpr int BL_THREADS = 256;
+constexpr int BL_MAX_CTAS = 32;
+constexpr int BL_WMAX = 8;
+
 __device__ __forceinline__ uint32_t row_word(const MaskSet& ms, int r, int u, int w, int W) {
   uint32_t x = 0;
   for (int i = 0; i < ms.n; ++i)
@@ -187,70 +247,97 @@ __device__ __forceinline__ uint32_t row_word(const MaskSet& ms, int r, int u, in
   return x;
 }
 
-__global__ void __launch_bounds__(1024) build_lists_kernel(int rows, int g_q, int g_kv, MaskSet ms,
-                                                           int* __restrict__ row_ptr,
-                                                           int* __restrict__ col_idx,
-                                                           long long cap, int* status) {
+__device__ __forceinline__ int block_sum(int v, int* s_warp) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  __syncthreads();
+  if (lane == 0) s_warp[warp] = v;
+  __syncthreads();
+  int tot = 0;
+  for (int i = 0; i < nw; ++i) tot += s_warp[i];
+  return tot;
+}
+
+__global__ void __launch_bounds__(BL_THREADS) build_lists_kernel(int rows, int g_q, int g_kv,
+                                                                 MaskSet ms, int* __restrict__ row_ptr,
+                                                                 int* __restrict__ col_idx,
+                                                                 long long cap, int* status,
+                                                                 int rows_per_cta) {
   __shared__ int s_warp[32];
-  __shared__ int s_carry;
-  __shared__ int s_err;
+  __shared__ int s_off[BL_THREADS + 1];
+  __shared__ uint32_t s_words[BL_THREADS * BL_WMAX];   // the chunk's OR-ed rows (W <= BL_WMAX)
   const int W = (g_kv + 31) / 32;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
-  if (threadIdx.x == 0) {
-    s_carry = 0;
-    s_err = 0;
-    row_ptr[0] = 0;
-  }
-  __syncthreads();
-  for (int base = 0; base < rows; base += blockDim.x) {
-    const int r = base + threadIdx.x;
-    int c = 0;
-    if (r < rows) {
-      const int u = r % g_q;
-      for (int w = 0; w < W; ++w) c += __popc(row_word(ms, r, u, w, W));
-      if (c == 0) s_err = 5;                               // SPARVAR_ERR_EMPTY_ROW
+  const int r0 = blockIdx.x * rows_per_cta;
+  const int r1 = min(rows, r0 + rows_per_cta);
+  if (r0 >= r1) return;
+  // base offset: set bits of rows [0, r0)
+  int mine = 0;
+  // rows [0, r0), 4 rows per thread per round so several loads are in flight
+  for (int rb = threadIdx.x; rb < r0; rb += 4 * blockDim.x) {
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int r = rb + q * blockDim.x;
+      if (r < r0) {
+        const int u = r % g_q;
+        for (int w = 0; w < W; ++w) mine += __popc(row_word(ms, r, u, w, W));
+      }
     }
+  }
+  long long base = block_sum(mine, s_warp);
+  if (blockIdx.x == 0 && threadIdx.x == 0) row_ptr[0] = 0;
+  int err = 0;
+  for (int c0 = r0; c0 < r1; c0 += blockDim.x) {
+    const int r = c0 + threadIdx.x;
+    int c = 0;
+    if (r < r1) {
+      for (int w = 0; w < W; ++w) {
+        const uint32_t x = row_word(ms, r, r % g_q, w, W);
+        if (W <= BL_WMAX) s_words[threadIdx.x * BL_WMAX + w] = x;
+        c += __popc(x);
+      }
+      if (c == 0) err = 5;                                  // SPARVAR_ERR_EMPTY_ROW
+    }
+    // block exclusive scan of c
     int inc = c;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
       const int t = __shfl_up_sync(0xffffffffu, inc, o);
       if (lane >= o) inc += t;
     }
+    __syncthreads();
     if (lane == 31) s_warp[warp] = inc;
     __syncthreads();
-    if (warp == 0) {
-      int wv = lane < nw ? s_warp[lane] : 0;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const int t = __shfl_up_sync(0xffffffffu, wv, o);
-        if (lane >= o) wv += t;
-      }
-      s_warp[lane] = wv;
+    int wpre = 0, tot = 0;
+    for (int i = 0; i < nw; ++i) {
+      if (i < warp) wpre += s_warp[i];
+      tot += s_warp[i];
     }
+    const int excl = wpre + inc - c;
+    s_off[threadIdx.x] = excl;
+    if (threadIdx.x == 0) s_off[blockDim.x] = tot;
+    if (r < r1) row_ptr[r + 1] = (int)(base + excl + c);
     __syncthreads();
-    const int pre = (warp > 0 ? s_warp[warp - 1] : 0) + s_carry;
-    if (r < rows) row_ptr[r + 1] = pre + inc;
-    __syncthreads();
-    if (threadIdx.x == blockDim.x - 1) s_carry = pre + inc;
-    __syncthreads();
-  }
-  const long long nnz = s_carry;
-  if (nnz > cap) {
-    if (threadIdx.x == 0 && status) atomicCAS(status, 0, 4);   // SPARVAR_ERR_CAPACITY
-    return;
-  }
-  if (threadIdx.x == 0 && status && s_err) atomicCAS(status, 0, s_err);
-  for (int r = threadIdx.x; r < rows; r += blockDim.x) {
-    const int u = r % g_q;
-    int pos = row_ptr[r];
-    for (int w = 0; w < W; ++w) {
-      uint32_t x = row_word(ms, r, u, w, W);
-      while (x) {
-        col_idx[pos++] = w * 32 + __ffs(x) - 1;
-        x &= x - 1;
+    if (base + tot > cap) {
+      if (threadIdx.x == 0 && status) atomicCAS(status, 0, 4);   // SPARVAR_ERR_CAPACITY
+      return;
+    }
+    // one warp per row: coalesced list stores
+    for (int rr = warp; rr < min((int)blockDim.x, r1 - c0); rr += nw) {
+      const int row = c0 + rr;
+      long long pos = base + s_off[rr];
+      for (int w = 0; w < W; ++w) {
+        const uint32_t x = W <= BL_WMAX ? s_words[rr * BL_WMAX + w]   // warp-uniform
+                                        : row_word(ms, row, row % g_q, w, W);
+        if ((x >> lane) & 1u) col_idx[pos + __popc(x & ((1u << lane) - 1u))] = w * 32 + lane;
+        pos += __popc(x);
       }
     }
+    base += tot;
+    __syncthreads();
   }
+  if (err && status) atomicCAS(status, 0, err);
 }
 
 }  // namespace
@@ -296,22 +383,33 @@ cudaError_t launch_map_indices(const Geo& g, int S, int K, int block, int sink_s
                                                                 G_S, G_K, W_S, W_K, src, dst);
     return cudaGetLastError();
   }
-  if (smem > 48 * 1024) {
-    cudaError_t e = cudaFuncSetAttribute(map_table_kernel,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-  }
   // Enough CTAs to cover the SMs; each CTA rebuilds the (identical) table for its (b,h) range.
   const int bh_per_cta = bh <= 148 ? 1 : (bh + 147) / 148;
   const int ctas = (bh + bh_per_cta - 1) / bh_per_cta;
-  map_table_kernel<<<ctas, 256, smem, st>>>(g, S, K, block, sink_scales, mode, G_S, G_K, G_kvS,
-                                            W_S, W_K, bh, bh_per_cta, src, dst);
-  return cudaGetLastError();
+  auto launch = [&](auto kern) -> cudaError_t {
+    if (smem > 48 * 1024) {
+      cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           (int)smem);
+      if (e != cudaSuccess) return e;
+    }
+    kern<<<ctas, 1024, smem, st>>>(g, S, K, block, sink_scales, mode, G_S, G_K, G_kvS, W_S, W_K,
+                                  bh, bh_per_cta, src, dst);
+    return cudaGetLastError();
+  };
+  if (W_K <= 4) return launch(map_table_kernel<4>);
+  if (W_K <= 8) return launch(map_table_kernel<8>);
+  return launch(map_table_kernel<0>);
 }
 
 cudaError_t launch_build_lists(int bh, int g_q, int g_kv, const MaskSet& ms, int* row_ptr,
                                int* col_idx, long long cap, int* status, cudaStream_t st) {
-  build_lists_kernel<<<1, 1024, 0, st>>>(bh * g_q, g_q, g_kv, ms, row_ptr, col_idx, cap, status);
+  const int rows = bh * g_q;
+  int ctas = (rows + 63) / 64;
+  if (ctas > BL_MAX_CTAS) ctas = BL_MAX_CTAS;
+  const int per = (rows + ctas - 1) / ctas;
+  ctas = (rows + per - 1) / per;
+  build_lists_kernel<<<ctas, BL_THREADS, 0, st>>>(rows, g_q, g_kv, ms, row_ptr, col_idx, cap, status,
+                                                  per);
   return cudaGetLastError();
 }
 

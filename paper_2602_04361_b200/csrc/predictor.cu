@@ -6,89 +6,130 @@
 //     mass[u, v] = sum_{q in u} sum_{j in v, j < C_S} P[q, j]
 //     keep TOPK(k) (ties to the smaller v) or mass >= tau * |u|, then OR the sink blocks.
 //
-// One pass: a CTA owns a 128-row Q tile (G = 128/B query blocks).  Warp 0 streams K blocks with
-// TMA, warp 1 issues S_j = Q K_j^T into one of two TMEM buffers (so QK of step j+1 overlaps the
-// softmax of step j), warps 2-5 (one query row per thread) keep, for every KV block j, the
-// block-local max m_j and sum_j = sum exp2(s*scale*log2e - m_j) in shared memory.  At the end
-// each row rescales them to its final max/normaliser (exact: P = 2^(s' - m_j) 2^(m_j - m) / l),
-// rows are reduced per query block in a fixed order (deterministic), and one warp per query block
-// selects with ballots into bit rows.
+// Design (DESIGN.md §7 "predict_kernel"):
+//  * Persistent, one CTA per SM, two tile SLOTS (128 query rows each) with their own softmax
+//    warpgroup and a double-buffered S in TMEM (4 x 128 columns): the tensor core computes
+//    S_{j+1} while the softmax warps reduce S_j, so the kernel runs at the exp2 throughput.
+//  * Every tile has the same G_kvS KV steps, so the MMA warp and the K loader alternate the two
+//    slots in lockstep; when both slots work on the same (b,h) they share each K stage.
+//  * Per (row, KV block) the softmax warps keep the block sum of 2^(s*scale*log2e - m) relative
+//    to the row's running max m (lazy: the stored sums are rescaled only when m grows by more
+//    than 2^8).  At the tile end each row normalises by l = sum of its block sums (exact:
+//    P[q, j] = 2^(s' - m) / l), rows are reduced per query block in a fixed order
+//    (deterministic), and one warp per query block selects with ballots into bit rows.
+//  * A fraction of the exp2 runs as a degree-4 polynomial on the FMA pipe (relative error
+//    2.6e-6, well inside the 1e-4 mass tolerance) to take load off the MUFU pipe.
 #include <cuda_bf16.h>
 #include <cstdio>
 
 #include "kernels.h"
 #include "ptx.cuh"
+#include "kernel_util.cuh"
+
+#ifndef SV_PRED_QB
+#define SV_PRED_QB 4     // preferred number of Q buffers (2..4); fewer if shared memory is short
+#endif
+#ifndef SV_PRED_EMU_EVERY
+#define SV_PRED_EMU_EVERY 0   // measured: FMA-pipe exp2 slows this kernel down
+#endif
 
 namespace sv {
 namespace {
 
 constexpr int BM = 128;
-constexpr int NUM_THREADS = 192;
-constexpr uint32_t TMEM_COLS = 256;
+constexpr int NUM_WARPS = 12;            // WG0/WG1 softmax slot 0/1, warp 8 MMA, 9 K, 10 Q
+constexpr int NUM_THREADS = NUM_WARPS * 32;
+constexpr int WARP_MMA = 8, WARP_K = 9, WARP_Q = 10;
+constexpr int REG_LAUNCH = 168;
+constexpr int REG_SOFTMAX = 208;
+constexpr int REG_OTHER = 88;
+static_assert(8 * (REG_SOFTMAX - REG_LAUNCH) <= 4 * (REG_LAUNCH - REG_OTHER), "register pool");
+constexpr uint32_t TMEM_COLS = 512;
+constexpr int EMU_EVERY = SV_PRED_EMU_EVERY;
+constexpr int SMEM_LIMIT = 232448;
+constexpr int MAXQ = 4;
+constexpr int NBARS = 2 * MAXQ + 2 * 8 + 8;   // q full/empty, kv full/empty, s full/free [2][2]
 
 template <int D, int BLK>
 struct PCfg {
   static constexpr int NBOX = D / 64;
   static constexpr int Q_BYTES = BM * D * 2;
   static constexpr int STAGE_BYTES = BLK * D * 2;
-  static constexpr int NST = (2 * 32768 / STAGE_BYTES) > 8 ? 8 : (2 * 32768 / STAGE_BYTES);
-  static constexpr int G = BM / BLK;
+  static constexpr int G = BM / BLK;                     // query blocks per tile
   static constexpr int SEG = BLK < 32 ? BLK : 32;        // rows reduced by one shuffle segment
   static constexpr int NSEG = BM / SEG;
-  static size_t smem(int g_kv) {
-    return 1024 + Q_BYTES + NST * STAGE_BYTES + 256 + size_t(2) * g_kv * BM * 4 +
-           size_t(NSEG) * g_kv * 4;
+  // bytes of everything but the Q buffers and the K ring
+  static size_t fixed(int g_kv) {
+    return size_t(2) * g_kv * BM * 4 /* block sums */ + size_t(2) * NSEG * g_kv * 4 /* parts */ +
+           NBARS * 8 + 16;
+  }
+  // (Q buffers, K stages) that fit, preferring 4 Q buffers (both tiles of the next round
+  // prefetched); nst = 0 if nothing fits
+  static void plan(int g_kv, int& nqb, int& nst) {
+    for (nqb = SV_PRED_QB; nqb >= 2; --nqb) {
+      const long long left = SMEM_LIMIT - (long long)fixed(g_kv) - (long long)nqb * Q_BYTES;
+      nst = left > 0 ? (int)(left / STAGE_BYTES) : 0;
+      if (nst > 8) nst = 8;
+      if (nst >= 2) return;
+    }
+    nst = 0;
+  }
+  static size_t smem(int g_kv, int nqb, int nst) {
+    return size_t(nqb) * Q_BYTES + size_t(nst) * STAGE_BYTES + fixed(g_kv);
   }
 };
-
-__device__ __forceinline__ void named_bar(int id, int n) {
-  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
-}
 
 template <int D, int BLK>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
 predict_kernel(const __grid_constant__ CUtensorMap tmap_q,
-               const __grid_constant__ CUtensorMap tmap_k, const PredArgs a) {
+               const __grid_constant__ CUtensorMap tmap_k, const PredArgs a, int nqb, int nst) {
   using C = PCfg<D, BLK>;
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
-                                             ~uintptr_t(1023));
+  extern __shared__ __align__(1024) uint8_t smem[];
+  const int n = a.g_kv;                                  // KV steps of every tile
   uint8_t* sQ = smem;
-  uint8_t* sK = smem + C::Q_BYTES;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sK + C::NST * C::STAGE_BYTES);
-  uint64_t* bar_q = bars;
-  uint64_t* bar_full = bars + 1;
-  uint64_t* bar_empty = bars + 1 + C::NST;
-  uint64_t* bar_s = bars + 1 + 2 * C::NST;     // [2]
-  uint64_t* bar_free = bar_s + 2;              // [2]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar_free + 2);
-  float* st_m = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(bars) + 256);
-  float* st_s = st_m + a.g_kv * BM;
-  float* part = st_s + a.g_kv * BM;            // [NSEG][g_kv]
+  uint8_t* sK = smem + nqb * C::Q_BYTES;
+  float* sums = reinterpret_cast<float*>(sK + nst * C::STAGE_BYTES);   // [2][n][BM]
+  float* part = sums + 2 * n * BM;                                      // [2][NSEG][n]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(part + 2 * C::NSEG * n);
+  uint64_t* q_full = bars;           // [MAXQ]
+  uint64_t* q_empty = q_full + MAXQ; // [MAXQ]
+  uint64_t* kv_full = q_empty + MAXQ;// [8]
+  uint64_t* kv_empty = kv_full + 8;  // [8]
+  uint64_t* s_full = kv_empty + 8;   // [2 slots][2 bufs]
+  uint64_t* s_free = s_full + 4;     // [2 slots][2 bufs] (128 arrivals)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + NBARS);
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
-  const int tile = blockIdx.x;
-  const int bh = blockIdx.y;
-  const int n = a.g_kv;
+  const int n_tiles = (a.n_q + BM - 1) / BM;
+  const int items = n_tiles * a.bh;
+  // contiguous, equal-size range of tiles (every tile costs the same n steps)
+  const int lo = (int)((long long)items * blockIdx.x / gridDim.x);
+  const int hi = (int)((long long)items * (blockIdx.x + 1) / gridDim.x);
+  const int T = hi - lo;
 
   if (threadIdx.x == 0) {
-    mbar_init(bar_q, 1);
-    for (int i = 0; i < C::NST; ++i) {
-      mbar_init(bar_full + i, 1);
-      mbar_init(bar_empty + i, 1);
+    if ((smem_u32(smem) & 1023u) != 0) {
+      printf("sparvar: dynamic shared memory not 1024-byte aligned\n");
+      __trap();
     }
-    for (int i = 0; i < 2; ++i) {
-      mbar_init(bar_s + i, 1);
-      mbar_init(bar_free + i, BM);
+    for (int i = 0; i < MAXQ; ++i) {
+      mbar_init(q_full + i, 1);
+      mbar_init(q_empty + i, 1);
+    }
+    for (int i = 0; i < 8; ++i) {
+      mbar_init(kv_full + i, 1);
+      mbar_init(kv_empty + i, 1);
+    }
+    for (int i = 0; i < 4; ++i) {
+      mbar_init(s_full + i, 1);
+      mbar_init(s_free + i, BM);
     }
     fence_barrier_init();
   }
-  if (warp == 0 && lane == 0) {
-    prefetch_tmap(&tmap_q);
-    prefetch_tmap(&tmap_k);
-  }
-  if (warp == 1) {
+  if (warp == WARP_K && lane == 0) prefetch_tmap(&tmap_k);
+  if (warp == WARP_Q && lane == 0) prefetch_tmap(&tmap_q);
+  if (warp == WARP_MMA) {
     tmem_alloc(tmem_slot, TMEM_COLS);
     tmem_relinquish();
   }
@@ -96,166 +137,275 @@ predict_kernel(const __grid_constant__ CUtensorMap tmap_q,
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  // tile k of this CTA (item lo + k) runs in slot k & 1, round k >> 1; Q buffer k % nqb.
+  // Both slots of a round start and end together (equal step counts).
 
-  if (warp == 0) {
-    if (lane == 0) {
-      mbar_arrive_expect_tx(bar_q, C::Q_BYTES);
+  if (warp >= 8) {
+    reg_dealloc<REG_OTHER>();
+    if (warp == WARP_Q) {
+      // ---------------------------------------------------------------- Q loader
+      if (lane == 0) {
+        for (int k = 0; k < T; ++k) {
+          const int b = k % nqb;
+          if (k >= nqb) mbar_wait(q_empty + b, ((k / nqb) - 1) & 1);
+          const int it = lo + k;
+          mbar_arrive_expect_tx(q_full + b, C::Q_BYTES);
 #pragma unroll
-      for (int b = 0; b < C::NBOX; ++b)
-        tma_load_3d(sQ + b * (BM * 128), &tmap_q, bar_q, b * 64, tile * BM, bh);
-      for (int j = 0; j < n; ++j) {
-        const int st = j % C::NST;
-        const uint32_t ph = (j / C::NST) & 1;
-        mbar_wait(bar_empty + st, ph ^ 1);
-        mbar_arrive_expect_tx(bar_full + st, C::STAGE_BYTES);
-#pragma unroll
-        for (int b = 0; b < C::NBOX; ++b)
-          tma_load_3d(sK + st * C::STAGE_BYTES + b * (BLK * 128), &tmap_k, bar_full + st, b * 64,
-                      j * BLK, bh);
-      }
-    }
-  } else if (warp == 1) {
-    if (lane == 0) {
-      constexpr uint32_t IDESC = idesc_bf16_f32(BM, BLK, 0, 0);
-      const uint32_t q_base = smem_u32(sQ);
-      const uint32_t k_base = smem_u32(sK);
-      mbar_wait(bar_q, 0);
-      tc_fence_after();
-      for (int j = 0; j < n; ++j) {
-        const int st = j % C::NST;
-        const uint32_t ph = (j / C::NST) & 1;
-        const int buf = j & 1;
-        mbar_wait(bar_free + buf, ((j >> 1) & 1) ^ 1);   // softmax done with S[buf] of step j-2
-        mbar_wait(bar_full + st, ph);
-        tc_fence_after();
-        const uint32_t kb = k_base + st * C::STAGE_BYTES;
-#pragma unroll
-        for (int kk = 0; kk < D / 16; ++kk) {
-          const uint64_t da = sdesc_sw128(q_base + (kk >> 2) * (BM * 128) + (kk & 3) * 32, 16, 1024);
-          const uint64_t db = sdesc_sw128(kb + (kk >> 2) * (BLK * 128) + (kk & 3) * 32, 16, 1024);
-          mma_ss(tmem + buf * 128, da, db, IDESC, kk > 0);
+          for (int x = 0; x < C::NBOX; ++x)
+            tma_load_3d(sQ + b * C::Q_BYTES + x * (BM * 128), &tmap_q, q_full + b, x * 64,
+                        (it % n_tiles) * BM, it / n_tiles);
         }
-        mma_commit(bar_empty + st);
-        mma_commit(bar_s + buf);
+      }
+    } else if (warp == WARP_K) {
+      // ---------------------------------------------------------------- K loader
+      if (lane == 0) {
+        const uint64_t pol = policy_evict_last();
+        int idx = 0;
+        for (int r = 0; 2 * r < T; ++r) {
+          const int bh0 = (lo + 2 * r) / n_tiles;
+          const bool two = 2 * r + 1 < T;
+          const bool shared = two && (lo + 2 * r + 1) / n_tiles == bh0;
+          for (int j = 0; j < n; ++j) {
+            for (int t = 0; t < (two && !shared ? 2 : 1); ++t) {
+              const int bh = (lo + 2 * r + t) / n_tiles;
+              const int s = idx % nst;
+              const uint32_t ph = (idx / nst) & 1;
+              ++idx;
+              mbar_wait(kv_empty + s, ph ^ 1);
+              mbar_arrive_expect_tx(kv_full + s, C::STAGE_BYTES);
+#pragma unroll
+              for (int x = 0; x < C::NBOX; ++x)
+                tma_load_3d_hint(sK + s * C::STAGE_BYTES + x * (BLK * 128), &tmap_k, kv_full + s,
+                                 x * 64, j * BLK, bh, pol);
+            }
+          }
+        }
+      }
+    } else if (warp == WARP_MMA) {
+      // ---------------------------------------------------------------- tcgen05 issuer
+      constexpr uint32_t IDESC = idesc_bf16_f32(BM, BLK, 0, 0);
+      const bool leader = elect_one();
+      const uint64_t dq0 = sdesc_sw128(smem_u32(sQ), 16, 1024);
+      const uint64_t dk0 = sdesc_sw128(smem_u32(sK), 16, 1024);
+      int idx = 0;
+      uint32_t step0 = 0, step1 = 0;   // S buffer uses per slot
+      for (int r = 0; 2 * r < T; ++r) {
+        const bool two = 2 * r + 1 < T;
+        const bool shared = two && (lo + 2 * r + 1) / n_tiles == (lo + 2 * r) / n_tiles;
+        for (int t = 0; t < (two ? 2 : 1); ++t) {
+          const int k = 2 * r + t;
+          mbar_wait(q_full + k % nqb, (k / nqb) & 1);
+        }
+        for (int j = 0; j < n; ++j) {
+          int s = 0;
+          for (int t = 0; t < (two ? 2 : 1); ++t) {
+            const int k = 2 * r + t;
+            const uint32_t g = t ? step1 : step0;
+            if (t) ++step1; else ++step0;
+            const int buf = g & 1;
+            // softmax of this slot is done reading S[buf] (step g - 2)
+            mbar_wait(s_free + 2 * t + buf, ((g >> 1) & 1) ^ 1);
+            if (t == 0 || !shared) {
+              s = idx % nst;
+              mbar_wait(kv_full + s, (idx / nst) & 1);
+              ++idx;
+            }
+            tc_fence_after();
+            const uint64_t da = dq0 + ((uint64_t)((k % nqb) * C::Q_BYTES) >> 4);
+            const uint64_t db = dk0 + ((uint64_t)(s * C::STAGE_BYTES) >> 4);
+            if (leader) {
+#pragma unroll
+              for (int kk = 0; kk < D / 16; ++kk) {
+                const uint32_t oa = ((kk >> 2) * (BM * 128) + (kk & 3) * 32) >> 4;
+                const uint32_t ob = ((kk >> 2) * (BLK * 128) + (kk & 3) * 32) >> 4;
+                mma_ss(tmem + (2 * t + buf) * 128, da + oa, db + ob, IDESC, kk > 0);
+              }
+              if (t == 1 || !shared || !two) mma_commit(kv_empty + s);
+              mma_commit(s_full + 2 * t + buf);
+              if (j == n - 1) mma_commit(q_empty + k % nqb);
+            }
+            __syncwarp();
+          }
+        }
       }
     }
+    reg_alloc<REG_LAUNCH>();
   } else {
+    // ---------------------------------------------------------------- softmax warpgroups
+    reg_alloc<REG_SOFTMAX>();
+    const int t = warp >> 2;
     const int quarter = warp & 3;
     const int row = quarter * 32 + lane;
     const uint32_t t_row = tmem + (uint32_t(quarter * 32) << 16);
     const float sl2 = a.scale_log2;
-    for (int j = 0; j < n; ++j) {
-      const int buf = j & 1;
-      mbar_wait(bar_s + buf, (j >> 1) & 1);
-      tc_fence_after();
-      uint32_t sr[BLK];
-      if constexpr (BLK >= 32) {
+    const uint64_t sl2x2 = f2_pack(sl2, sl2);
+    float* my_sums = sums + t * n * BM;
+    float* my_part = part + t * C::NSEG * n;
+    uint32_t g = 0;
+    for (int k = t; k < T; k += 2) {
+      const int it = lo + k;
+      const int bh = it / n_tiles, tile = it % n_tiles;
+      float m = -INFINITY;
+      for (int j = 0; j < n; ++j, ++g) {
+        const int buf = g & 1;
+        mbar_wait(s_full + 2 * t + buf, (g >> 1) & 1);
+        tc_fence_after();
+        uint32_t sr[BLK];
+        if constexpr (BLK >= 32) {
 #pragma unroll
-        for (int c = 0; c < BLK; c += 32) tmem_ld32(t_row + buf * 128 + c, sr + c);
-      } else {
+          for (int c = 0; c < BLK; c += 32) tmem_ld32(t_row + (2 * t + buf) * 128 + c, sr + c);
+        } else {
 #pragma unroll
-        for (int c = 0; c < BLK; c += 8) tmem_ld8(t_row + buf * 128 + c, sr + c);
-      }
-      tmem_wait_ld();
-      tc_fence_before();
-      mbar_arrive(bar_free + buf);
-      const int valid = min(BLK, a.n_kv - j * BLK);
-      float mx = -INFINITY;
-#pragma unroll
-      for (int c = 0; c < BLK; ++c)
-        if (c < valid) mx = fmaxf(mx, __uint_as_float(sr[c]));
-      const float mref = mx * sl2;
-      float sum = 0.f;
-#pragma unroll
-      for (int c = 0; c < BLK; ++c)
-        if (c < valid) sum += ex2(fmaf(__uint_as_float(sr[c]), sl2, -mref));
-      st_m[j * BM + row] = mref;
-      st_s[j * BM + row] = sum;
-    }
-    // final max / normaliser of this row, then its share of every block mass
-    float m = -INFINITY;
-    for (int j = 0; j < n; ++j) m = fmaxf(m, st_m[j * BM + row]);
-    float l = 0.f;
-    for (int j = 0; j < n; ++j) l += st_s[j * BM + row] * ex2(st_m[j * BM + row] - m);
-    const bool row_valid = tile * BM + row < a.n_q;
-    const float inv = row_valid ? 1.f / l : 0.f;
-    // reduce over the rows of each query block, fixed order (deterministic)
-    for (int j = 0; j < n; ++j) {
-      float w = st_s[j * BM + row] * ex2(st_m[j * BM + row] - m) * inv;
-#pragma unroll
-      for (int off = C::SEG / 2; off > 0; off >>= 1) w += __shfl_xor_sync(0xffffffffu, w, off);
-      if ((lane % C::SEG) == 0) part[(row / C::SEG) * n + j] = w;
-    }
-    named_bar(1, BM);
-    // selection: one softmax warp per query block (loop)
-    const int W = (n + 31) / 32;
-    constexpr int SEG_PER_G = BLK / C::SEG;
-    for (int g = quarter; g < C::G; g += 4) {
-      const int u = tile * C::G + g;
-      if (u >= a.g_q) continue;
-      // mass of block v = sum of its segments, fixed order; stored into st_m (free now)
-      float* mrow = st_m + g * n;
-      for (int v = lane; v < n; v += 32) {
-        float acc = 0.f;
-        for (int sgi = 0; sgi < SEG_PER_G; ++sgi) acc += part[(g * SEG_PER_G + sgi) * n + v];
-        mrow[v] = acc;
-      }
-      __syncwarp();
-      const long long r = (long long)bh * a.g_q + u;
-      const int rows_u = min(BLK, a.n_q - u * BLK);
-      const float thr = a.tau * float(rows_u);
-      for (int w0 = 0; w0 < W; ++w0) {
-        const int v = w0 * 32 + lane;
-        bool sel = false;
-        if (v < n) {
-          const float mv = mrow[v];
-          if (a.mode == 0) {
-            int rank = 0;
-            for (int t = 0; t < n; ++t) {
-              const float mt = mrow[t];
-              rank += (mt > mv) || (mt == mv && t < v);
-            }
-            sel = rank < a.topk;
-          } else {
-            sel = mv >= thr;
-          }
-          sel = sel || (v < a.n_sink_blocks);
-          if (a.mass) a.mass[r * n + v] = mv;
+          for (int c = 0; c < BLK; c += 8) tmem_ld8(t_row + (2 * t + buf) * 128 + c, sr + c);
         }
-        const uint32_t word = __ballot_sync(0xffffffffu, sel);
-        if (lane == 0) a.mask[r * W + w0] = word;
+        tmem_wait_ld();
+        tc_fence_before();
+        mbar_arrive(s_free + 2 * t + buf);
+        const int valid = min(BLK, a.n_kv - j * BLK);   // ragged last KV block (READING 20)
+        if (__builtin_expect(valid < BLK, 0)) {
+#pragma unroll
+          for (int c = 0; c < BLK; ++c)
+            if (c >= valid) sr[c] = __float_as_uint(-INFINITY);
+        }
+        float mm[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+#pragma unroll
+        for (int c = 0; c < BLK; c += 4) {
+          const int q = (c >> 2) & 3;
+          mm[q] = fmax3(mm[q], __uint_as_float(sr[c]), __uint_as_float(sr[c + 1]));
+          mm[q] = fmax3(mm[q], __uint_as_float(sr[c + 2]), __uint_as_float(sr[c + 3]));
+        }
+        const float mx_s = fmax3(fmaxf(mm[0], mm[1]), mm[2], mm[3]) * sl2;
+        if (mx_s > m + 8.0f) {
+          // lazy rescale of the row's stored block sums (rare after the first blocks)
+          const float alpha = ex2(m - mx_s);
+          for (int jj = 0; jj < j; ++jj) my_sums[jj * BM + row] *= alpha;
+          m = mx_s;
+        }
+        const uint64_t negm = f2_pack(-m, -m);
+        uint64_t acc[4] = {0, 0, 0, 0};
+#pragma unroll
+        for (int c = 0; c < BLK; c += 2) {
+          const uint64_t x =
+              ffma2(f2_pack(__uint_as_float(sr[c]), __uint_as_float(sr[c + 1])), sl2x2, negm);
+          float p0, p1;
+          if (EMU_EVERY > 0 && valid == BLK &&
+              (c / 2) % (EMU_EVERY > 0 ? EMU_EVERY : 1) == EMU_EVERY - 1) {
+            ex2_emu2<4>(x, p0, p1);
+          } else {
+            float x0, x1;
+            f2_unpack(x, x0, x1);
+            p0 = ex2(x0);
+            p1 = ex2(x1);
+          }
+          acc[(c >> 1) & 3] = fadd2(acc[(c >> 1) & 3], f2_pack(p0, p1));
+        }
+        const uint64_t s2 = fadd2(fadd2(acc[0], acc[1]), fadd2(acc[2], acc[3]));
+        float s0, s1;
+        f2_unpack(s2, s0, s1);
+        my_sums[j * BM + row] = s0 + s1;
       }
+      // ------------------------------------------------------------ tile end: masses
+      float l = 0.f;
+      for (int j = 0; j < n; ++j) l += my_sums[j * BM + row];
+      const bool row_valid = tile * BM + row < a.n_q;
+      const float inv = row_valid ? 1.f / l : 0.f;
+      for (int j = 0; j < n; ++j) {
+        float w = my_sums[j * BM + row] * inv;
+#pragma unroll
+        for (int off = C::SEG / 2; off > 0; off >>= 1) w += __shfl_xor_sync(0xffffffffu, w, off);
+        if ((lane % C::SEG) == 0) my_part[(row / C::SEG) * n + j] = w;
+      }
+      named_bar(1 + t, BM);
+      // selection: one warp per query block; the block's mass row is staged in my_sums
+      const int W = (n + 31) / 32;
+      constexpr int SEG_PER_G = BLK / C::SEG;
+      for (int gq = quarter; gq < C::G; gq += 4) {
+        const int u = tile * C::G + gq;
+        if (u >= a.g_q) continue;
+        float* mrow = my_sums + gq * n;
+        for (int v = lane; v < n; v += 32) {
+          float acc = 0.f;
+          for (int sgi = 0; sgi < SEG_PER_G; ++sgi) acc += my_part[(gq * SEG_PER_G + sgi) * n + v];
+          mrow[v] = acc;
+        }
+        __syncwarp();
+        const long long r = (long long)bh * a.g_q + u;
+        const int rows_u = min(BLK, a.n_q - u * BLK);
+        const float thr = a.tau * float(rows_u);
+        for (int w0 = 0; w0 < W; ++w0) {
+          const int v = w0 * 32 + lane;
+          bool sel = false;
+          if (v < n) {
+            const float mv = mrow[v];
+            if (a.mode == 0) {
+              int rank = 0;
+              for (int tt = 0; tt < n; ++tt) {
+                const float mt = mrow[tt];
+                rank += (mt > mv) || (mt == mv && tt < v);
+              }
+              sel = rank < a.topk;
+            } else {
+              sel = mv >= thr;
+            }
+            sel = sel || (v < a.n_sink_blocks);
+            if (a.mass) a.mass[r * n + v] = mv;
+          }
+          const uint32_t word = __ballot_sync(0xffffffffu, sel);
+          if (lane == 0) a.mask[r * W + w0] = word;
+        }
+      }
+      named_bar(1 + t, BM);   // my_sums / my_part are reused by the next tile
     }
+    reg_dealloc<REG_LAUNCH>();
   }
 
   tc_fence_before();
   __syncthreads();
-  if (warp == 1) {
-    __syncwarp();
+  if (warp == WARP_MMA) {
     tc_fence_after();
     tmem_dealloc(tmem, TMEM_COLS);
   }
+}
+
+int num_sms_pred() {
+  static int n = 0;
+  if (n == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n <= 0)
+      n = 148;
+  }
+  return n;
 }
 
 template <int D, int BLK>
 cudaError_t launch_t(const CUtensorMap& tq, const CUtensorMap& tk, const PredArgs& a,
                      cudaStream_t st) {
   using C = PCfg<D, BLK>;
-  const size_t smem = C::smem(a.g_kv);
-  if (smem > 227 * 1024) return cudaErrorInvalidValue;
+  int nqb, nst;
+  C::plan(a.g_kv, nqb, nst);
+  if (nst < 2) return cudaErrorInvalidValue;
+  const size_t smem = C::smem(a.g_kv, nqb, nst);
   auto kern = predict_kernel<D, BLK>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  dim3 grid((a.n_q + BM - 1) / BM, a.bh);
-  kern<<<grid, NUM_THREADS, smem, st>>>(tq, tk, a);
+  const long long items = (long long)((a.n_q + BM - 1) / BM) * a.bh;
+  if (items <= 0) return cudaSuccess;
+  const int sms = num_sms_pred();
+  const int grid = (int)(items >= 2LL * sms ? sms : (items + 1) / 2);
+  kern<<<grid, NUM_THREADS, smem, st>>>(tq, tk, a, nqb, nst);
   return cudaGetLastError();
 }
 
 }  // namespace
 
 size_t predictor_smem_bytes(int head_dim, int block, int g_kv) {
-#define SV_CASE(D_, B_) \
-  if (head_dim == D_ && block == B_) return PCfg<D_, B_>::smem(g_kv);
+#define SV_CASE(D_, B_)                            \
+  if (head_dim == D_ && block == B_) {             \
+    int nqb, nst;                                  \
+    PCfg<D_, B_>::plan(g_kv, nqb, nst);            \
+    return nst < 2 ? ~size_t(0) : PCfg<D_, B_>::smem(g_kv, nqb, nst); \
+  }
   SV_CASE(128, 128) SV_CASE(128, 64) SV_CASE(128, 32) SV_CASE(128, 16)
   SV_CASE(64, 128) SV_CASE(64, 64) SV_CASE(64, 32) SV_CASE(64, 16)
 #undef SV_CASE
