@@ -44,9 +44,18 @@ extern "C" int sparvar_prof_read(long long* host, int n) {
   if (blockIdx.x == 0 && threadIdx.x == 0 && (i_) < 7000) sv_prof_buf[(i_)] = clock64();
 #define SV_STAMP_CTA(base_) \
   if (threadIdx.x == 0 && blockIdx.x < 192) sv_prof_buf[(base_) + blockIdx.x] = (long long)globaltimer_ns();
+#define SV_ACC(base_, v_) \
+  if (blockIdx.x < 192) atomicAdd((unsigned long long*)&sv_prof_buf[(base_) + blockIdx.x], (unsigned long long)(v_));
+#define SV_CLK() clock64()
+extern "C" int sparvar_prof_reset() {
+  static long long z[8192];
+  return cudaMemcpyToSymbol(sv_prof_buf, z, sizeof(z)) == cudaSuccess ? 0 : 1;
+}
 #else
-#define SV_STAMP(i_)
-#define SV_STAMP_CTA(base_)
+#define SV_STAMP(i_) {}
+#define SV_STAMP_CTA(base_) {}
+#define SV_ACC(base_, v_) {}
+#define SV_CLK() 0LL
 #endif
 
 #ifndef SV_EMU_EVERY
@@ -71,11 +80,27 @@ static_assert(8 * (REG_SOFTMAX - REG_LAUNCH) <=
               "register pool");
 constexpr int EMU_EVERY = SV_EMU_EVERY;  // 1 in EMU_EVERY exp2 pairs on the FMA pipe (0 = none)
 constexpr uint32_t TMEM_COLS = 512;
-constexpr int NQB = 3;                   // Q buffers
+#ifndef SV_NQB
+#define SV_NQB 3
+#endif
+constexpr int NQB = SV_NQB;              // Q buffers
 constexpr int MAX_TILES = 96;            // tiles per schedule batch
 constexpr int TILE_OVERHEAD = 2;         // per-tile cost, in KV steps, for the balanced partition
 constexpr int SMEM_LIMIT = 232448;       // 227 KB opt-in
 constexpr uint8_t EMPTY_TILE = 0xFF;
+#ifndef SV_ORDER
+#define SV_ORDER 1
+#endif
+// Work order.  0: cost-balanced contiguous item ranges (one head per CTA at a time: every head is
+// active at once, K/V working set far above L2).  1: strided windows -- at any time the CTAs work
+// on ~grid consecutive items (a few heads, L2-resident K/V); CTA c takes position
+// (c + k*R) mod grid of window k so a CTA does not keep drawing the same query-tile index.
+constexpr int ORDER = SV_ORDER;
+
+__host__ __device__ inline int gcd_int(int a, int b) {
+  while (b) { const int t = a % b; a = b; b = t; }
+  return a;
+}
 
 // Small shared state after the Q / KV buffers.
 struct Small {
@@ -241,7 +266,7 @@ attn_fwd_kernel(const __grid_constant__ CUtensorMap tmap_q,
     tmem_alloc(&sm->tmem_slot, TMEM_COLS);
     tmem_relinquish();
   }
-  if (warp == 1) {
+  if (ORDER == 0 && warp == 1) {
     // balanced contiguous range [lo, hi) of this CTA: lanes 0-15 search the lower boundary,
     // lanes 16-31 the upper one, 16 probes per round (min i with F(i) >= target)
     const int N = item_end - item_begin;
@@ -283,7 +308,20 @@ attn_fwd_kernel(const __grid_constant__ CUtensorMap tmap_q,
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = sm->tmem_slot;
-  const int range_lo = sm->lo, range_hi = sm->hi;
+  // this CTA's items: item_at(li) for li in [0, n_mine), increasing
+  const int N_items = item_end - item_begin;
+  const int grid = gridDim.x;
+  int rot = 59;
+  while (gcd_int(rot % grid, grid) != 1 && grid > 1) rot += 2;
+  const int k_full = N_items / grid;
+  const int n_mine = ORDER == 0 ? sm->hi - sm->lo
+                                : k_full + (((blockIdx.x + (long long)k_full * rot) % grid) <
+                                                    N_items - k_full * grid ? 1 : 0);
+  const int range_lo = ORDER == 0 ? sm->lo : 0;
+  auto item_at = [&](int li) -> int {
+    if (ORDER == 0) return range_lo + li;
+    return item_begin + li * grid + (int)((blockIdx.x + (long long)li * rot) % grid);
+  };
   SV_STAMP_CTA(7600)
 
   // role state that persists across schedule batches (barrier phases, ring positions)
@@ -293,10 +331,10 @@ attn_fwd_kernel(const __grid_constant__ CUtensorMap tmap_q,
   uint32_t s_cnt = 0;              // softmax: S phases consumed
   uint32_t q_used = 0;             // Q loader: buffers used at least once (bits)
 
-  for (int b0 = range_lo; b0 < range_hi; b0 += MAX_TILES) {
-    const int T = min(MAX_TILES, range_hi - b0);
+  for (int b0 = 0; b0 < n_mine; b0 += MAX_TILES) {
+    const int T = min(MAX_TILES, n_mine - b0);
     for (int i = threadIdx.x; i < T; i += NUM_THREADS) {
-      const int it = b0 + i;
+      const int it = item_at(b0 + i);
       Steps<G> st;
       st.init(a, it / n_tiles, it % n_tiles, g_kv);
       sm->n[i] = (uint16_t)st.count(a);
@@ -328,6 +366,8 @@ attn_fwd_kernel(const __grid_constant__ CUtensorMap tmap_q,
         int buf;
         if (k < NQB) {
           buf = k;
+        } else if (NQB == 2) {
+          buf = r0 <= r1 ? 0 : 1;
         } else {
           buf = (r0 <= r1 && r0 <= r2) ? 0 : (r1 <= r2 ? 1 : 2);
         }
@@ -362,7 +402,7 @@ attn_fwd_kernel(const __grid_constant__ CUtensorMap tmap_q,
       for (int e = 0; e < Tn; ++e) {
         const int i = sm->eord[e];
         const int t = sm->meta[i] & 1;
-        const int it = b0 + i;
+        const int it = item_at(b0 + i);
         const int bh = it / n_tiles, tile = it % n_tiles;
         const uint32_t par = (t ? tiles1 : tiles0) & 1;
         if (t) ++tiles1; else ++tiles0;
@@ -420,7 +460,7 @@ attn_fwd_kernel(const __grid_constant__ CUtensorMap tmap_q,
             while (i < T && (sm->meta[i] == EMPTY_TILE || (sm->meta[i] & 1) != t)) ++i;
             icur[t] = i < T ? i : -1;
             if (icur[t] < 0) return;
-            const int it = b0 + i;
+            const int it = item_at(b0 + i);
             bhs[t] = it / n_tiles;
             st[t].init(a, bhs[t], it % n_tiles, g_kv);
             nn[t] = sm->n[i];
@@ -455,7 +495,7 @@ attn_fwd_kernel(const __grid_constant__ CUtensorMap tmap_q,
             const uint32_t use_par = (meta >> 3) & 1;
             if (q_used & (1u << buf)) mbar_wait(q_empty + buf, use_par ^ 1);
             q_used |= 1u << buf;
-            const int it = b0 + i;
+            const int it = item_at(b0 + i);
             uint8_t* dst = sQ + buf * C::Q_BYTES;
             mbar_arrive_expect_tx(q_full + buf, C::Q_BYTES);
 #pragma unroll
@@ -469,7 +509,7 @@ attn_fwd_kernel(const __grid_constant__ CUtensorMap tmap_q,
         // no listed block in any of the tile's query blocks: zero output, lse = -inf
         for (int i = 0; i < T; ++i) {
           if (sm->meta[i] != EMPTY_TILE) continue;
-          const int it = b0 + i;
+          const int it = item_at(b0 + i);
           const int bh = it / n_tiles, tile = it % n_tiles;
           for (int r = lane; r < BM; r += 32) {
             const int row = tile * BM + r;
@@ -597,7 +637,7 @@ attn_fwd_kernel(const __grid_constant__ CUtensorMap tmap_q,
       for (int i = 0; i < T; ++i) {
         const int meta = sm->meta[i];
         if (meta == EMPTY_TILE || (meta & 1) != t) continue;
-        const int it = b0 + i;
+        const int it = item_at(b0 + i);
         Steps<G> st;
         st.init(a, it / n_tiles, it % n_tiles, g_kv);
         float m = -INFINITY;   // running max of s * scale * log2(e)

@@ -22,6 +22,9 @@ fn = (lambda: sv.dense_attn(sides, K, q, k, v)) if which == "dense" else \
 for _ in range(3):
     fn()
 torch.cuda.synchronize()
+sv.lib.sparvar_prof_reset()
+fn()
+torch.cuda.synchronize()
 buf = (ctypes.c_longlong * 8192)()
 sv.lib.sparvar_prof_read.argtypes = [ctypes.c_void_p, ctypes.c_int]
 sv.lib.sparvar_prof_read(buf, 8192)
@@ -44,3 +47,15 @@ if st0.min() > 0:
     print("CTA start spread us: %.2f   setup (median) us: %.2f   end: min %.2f median %.2f max %.2f us" % (
         (st0.max() - t0) / 1e3, np.median(su - st0) / 1e3, (en.min() - t0) / 1e3, np.median(en - t0) / 1e3,
         (en.max() - t0) / 1e3))
+
+def cta(base):
+    return a[base:base + 148].astype(np.float64)
+sm_wait, sm_tot = cta(5000), cta(5200)
+pw, kw, ow, qw, mt = cta(5400), cta(5600), cta(5800), cta(6000), cta(6200)
+print("per-CTA medians (clk): softmax(slot0,thr0) total %.0f wait-S %.0f (%.0f%%)" % (
+    np.median(sm_tot), np.median(sm_wait), 100 * np.median(sm_wait / np.maximum(sm_tot, 1))))
+print("  MMA total %.0f: wait P %.0f (%.0f%%)  wait KV %.0f (%.0f%%)  wait O-free %.0f  wait Q %.0f" % (
+    np.median(mt), np.median(pw), 100 * np.median(pw / np.maximum(mt, 1)), np.median(kw),
+    100 * np.median(kw / np.maximum(mt, 1)), np.median(ow), np.median(qw)))
+lt, lw = cta(6400), cta(6600)
+print("  KV loader total %.0f: wait empty stage %.0f (%.0f%%)" % (np.median(lt), np.median(lw), 100 * np.median(lw / np.maximum(lt, 1))))

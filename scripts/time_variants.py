@@ -30,7 +30,7 @@ except Exception:
     clk = lambda: -1
 res = {(n, w): [] for n in handles for w in nnz}
 clks = []
-for rep in range(5):
+for rep in range(7):
     for name, L in handles.items():
         sv.lib = L
         for w in ("csla", "cs4a", "dense"):
@@ -47,12 +47,12 @@ for rep in range(5):
             torch.cuda.synchronize()
             clks.append(clk())
             res[(name, w)].append(e0.elapsed_time(e1) / reps)
-print("SM clock MHz during runs: median %s min %s" % (statistics.median(clks), min(clks)))
+print("SM clock MHz during runs: median %s min %s  (times: min over 7 interleaved rounds)" % (statistics.median(clks), min(clks)))
 for name in handles:
     line = [name.ljust(18)]
     for w in ("csla", "cs4a", "dense"):
-        ms = statistics.median(res[(name, w)])
+        ms = min(res[(name, w)])
         line.append(f"{w} {ms:.4f} ms ({4 * D * B * B * nnz[w] / ms / 1e9:.0f} TF)")
-    d, c = statistics.median(res[(name, "dense")]), statistics.median(res[(name, "csla")])
+    d, c = min(res[(name, "dense")]), min(res[(name, "csla")])
     line.append(f"x{d / c:.2f}")
     print("  ".join(line), flush=True)
