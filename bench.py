@@ -215,11 +215,12 @@ def main():
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     import paper_2602_04361_b200 as sv
+    from paper_2602_04361_b200 import shard as sv_shard
     from synth import kv_cache_iid, q_iid
 
     cfg = CONFIGS[args.config]
     units = cfg["batch"] * cfg["heads"]
-    bh0 = rank * units
+    bh0, _ = sv_shard.weak_units(rank, units)
     n_q, n_qS = SIDES[K_T - 1] ** 2, SIDES[S_D - 1] ** 2
     n_kv = sum(s * s for s in SIDES[:K_T])
     dev = torch.device("cuda", local_rank)
@@ -268,10 +269,7 @@ def main():
     clk = clocks.stop()
     ms_step = t0.elapsed_time(t1) / args.steps
     attn_ms = statistics.mean(a.elapsed_time(b) for a, b in ev_attn)
-    if world > 1:
-        t = torch.tensor([ms_step, attn_ms], device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms_step, attn_ms = float(t[0]), float(t[1])
+    ms_step, attn_ms = sv_shard.max_over_ranks([ms_step, attn_ms], device=dev)
 
     # --- dense denominator (a7), same shape, separately timed
     for _ in range(2):
@@ -308,10 +306,7 @@ def main():
     e1.record(stream)
     torch.cuda.synchronize()
     e2e_step = e0.elapsed_time(e1) / ne
-    if world > 1:
-        t = torch.tensor([e2e_step], device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        e2e_step = float(t[0])
+    (e2e_step,) = sv_shard.max_over_ranks([e2e_step], device=dev)
     h2d = sum(x.numel() * x.element_size() for x in (hq, hqS, hk, hv))
     d2h = 2 * hq.numel() * hq.element_size()
 
@@ -332,11 +327,7 @@ def main():
     # --- validation all-gather (untimed): each rank's sampled output rows -> rank 0 vs oracle
     sample_rows = torch.tensor([0, 1, 2047, 4095], device=dev)
     samp = o_csla[0].index_select(0, sample_rows).float().contiguous()
-    if world > 1:
-        gath = torch.empty((world,) + tuple(samp.shape), device=dev)
-        dist.all_gather_into_tensor(gath, samp)
-    else:
-        gath = samp.unsqueeze(0)
+    gath = sv_shard.gather_to_root(samp)
     validation = None
     if rank == 0:
         from oracle.attention import block_sparse, merge_lists
