@@ -320,7 +320,11 @@ def main():
     exec_flops = 4 * D * BLOCK * BLOCK * nnz
     rp2 = layer.lists["cs4a"][0].cpu().numpy()
     pk, src = peaks()
-    peak_tf = float(pk.get("bf16_tflops", 1590.0))
+    # the attention launch is timed inside a long step (50 x ~1.3 ms of back-to-back kernels):
+    # the sustained (power-capped) cuBLAS figure is the matching denominator; the burst-based
+    # fraction is reported beside it
+    peak_tf = float(pk.get("bf16_tflops_sustained", 1400.0))
+    peak_burst = float(pk.get("bf16_tflops", 1590.0))
     achieved_tf = alg_flops / (attn_ms * 1e-3) / 1e12
     exec_tf = exec_flops / (attn_ms * 1e-3) / 1e12
 
@@ -373,9 +377,11 @@ def main():
                          "achieved": round(achieved_tf, 1), "peak": peak_tf, "unit": "TFLOP/s",
                          "frac": round(achieved_tf / peak_tf, 4),
                          "traffic": traffic_from_profile(),
-                         "peak_source": f"{src} bf16_tflops (burst)",
+                         "peak_source": f"{src} bf16_tflops_sustained (kernel timed inside a long step)",
+                         "frac_of_burst_peak": round(achieved_tf / peak_burst, 4),
                          "flops_per_launch": alg_flops, "launch_ms": round(attn_ms, 4)},
             "tensor_util_executed": round(exec_tf / peak_tf, 4),
+            "tensor_util_executed_burst": round(exec_tf / peak_burst, 4),
             "csla_attn_ms": round(attn_ms, 4), "dense_attn_ms": round(dense_ms, 4),
             "speedup_vs_dense": round(dense_ms / attn_ms, 3),
             "csla_active_blocks_per_head": nnz // units,

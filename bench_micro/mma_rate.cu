@@ -57,8 +57,12 @@ __global__ void __launch_bounds__(160, 1) k_mix(long long* out, int iters) {
   __shared__ uint64_t bar;
   __shared__ uint32_t tslot;
   __shared__ volatile int stop;
+  __shared__ uint64_t done;
+  __shared__ uint64_t never;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  if (threadIdx.x == 0) { mbar_init(&bar, 1); fence_barrier_init(); stop = 0; }
+  if (threadIdx.x == 0) { mbar_init(&bar, 1); mbar_init(&done, 1); mbar_init(&never, 1); fence_barrier_init(); stop = 0; }
+  __syncthreads();
+  if (threadIdx.x == 0) mbar_arrive(&done);   // phase 0 of `done` completes immediately
   if (warp == 0) { tmem_alloc(&tslot, 512); tmem_relinquish(); }
   tc_fence_before();
   __syncthreads();
@@ -70,16 +74,19 @@ __global__ void __launch_bounds__(160, 1) k_mix(long long* out, int iters) {
     constexpr uint32_t idp = idesc_bf16_f32(128, 128, 0, 1);
     const long long t0 = clock64();
     for (int it = 0; it < iters; ++it) {
+      const uint32_t bs = (MODE & 32) ? b + (it & 3) * 32768u : b;   // rotate 4 "stages"
 #pragma unroll
       for (int kk = 0; kk < 8; ++kk)
         mma_ss(tmem, sdesc_sw128(a + (kk >> 2) * 16384 + (kk & 3) * 32, 16, 1024),
-               sdesc_sw128(b + (kk >> 2) * 16384 + (kk & 3) * 32, 16, 1024), idq, kk > 0);
+               sdesc_sw128(bs + (kk >> 2) * 16384 + (kk & 3) * 32, 16, 1024), idq, kk > 0);
       mma_commit(&bar);
+      if (MODE & 16) { mbar_wait(&done, 0); tc_fence_after(); }
 #pragma unroll
       for (int kk = 0; kk < 8; ++kk)
-        mma_ts(tmem + 256, tmem + kk * 8, sdesc_sw128(b + kk * 2048, 16384, 1024), idp, 1);
+        mma_ts(tmem + 256, tmem + kk * 8, sdesc_sw128(((MODE & 32) ? b + ((it + 2) & 3) * 32768u : b) + kk * 2048, 16384, 1024), idp, 1);
       mma_commit(&bar);
       if (MODE & 4) { mbar_wait(&bar, 1); }   // two commits per iteration: parity returns
+      if (MODE & 8) { mbar_wait(&done, 0); tc_fence_after(); }   // completed barrier + fence
     }
     mma_commit(&bar);
     const long long t1 = clock64();
@@ -92,6 +99,103 @@ __global__ void __launch_bounds__(160, 1) k_mix(long long* out, int iters) {
       if (MODE & 1) { tmem_ld32(trow + 128, r); tmem_wait_ld(); }
       if (MODE & 2) { tmem_st32(trow + 160, r); tmem_wait_st(); }
     }
+  } else if (warp >= 1 && (MODE & 64)) {
+    // background warps polling an mbarrier phase that never completes (like waiting softmax warps)
+    const uint32_t nb = smem_u32(&never);
+    while (!stop) {
+      if (mbar_try_wait(nb, 0)) break;
+      if (MODE & 128) { if (lane == 0) { } }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) { tc_fence_after(); tmem_dealloc(tmem, 512); }
+}
+
+// LDTM latency while the tensor pipe is busy: thread 0 keeps issuing SS MMAs into columns
+// [0,128); warps 1-4 time "4 x tcgen05.ld 32x32b.x32 of columns [256,384) + wait::ld".
+__global__ void __launch_bounds__(160, 1) k_ldtm_under_mma(long long* out, int iters, int busy) {
+  extern __shared__ __align__(1024) uint8_t sm[];
+  __shared__ uint32_t tslot;
+  __shared__ volatile int stop;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) stop = 0;
+  if (warp == 0) { tmem_alloc(&tslot, 512); tmem_relinquish(); }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = tslot;
+  if (threadIdx.x == 0) {
+    const uint32_t a = smem_u32(sm), b = smem_u32(sm + 32768);
+    constexpr uint32_t idq = idesc_bf16_f32(128, 128, 0, 0);
+    while (!stop && busy) {
+#pragma unroll
+      for (int kk = 0; kk < 8; ++kk)
+        mma_ss(tmem, sdesc_sw128(a + (kk >> 2) * 16384 + (kk & 3) * 32, 16, 1024),
+               sdesc_sw128(b + (kk >> 2) * 16384 + (kk & 3) * 32, 16, 1024), idq, kk > 0);
+    }
+  } else if (warp >= 1) {
+    const uint32_t trow = tmem + (uint32_t(((warp - 1) & 3) * 32) << 16);
+    uint32_t r[128];
+    uint32_t acc = 0;
+    long long t0 = clock64();
+    for (int i = 0; i < iters; ++i) {
+      tmem_ld32(trow + 256, r);
+      tmem_ld32(trow + 288, r + 32);
+      tmem_ld32(trow + 320, r + 64);
+      tmem_ld32(trow + 352, r + 96);
+      tmem_wait_ld();
+      acc += r[0] ^ r[127];
+    }
+    long long t1 = clock64();
+    if (lane == 0 && warp == 1) { out[blockIdx.x] = (t1 - t0) / iters; out[200 + blockIdx.x] = acc; }
+    __syncwarp();
+    if (warp == 1 && lane == 0) stop = 1;
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) { tc_fence_after(); tmem_dealloc(tmem, 512); }
+}
+
+// Attention-kernel MMA sequence without any waits: two slots (S at cols 0 / 128, O at 256 /
+// 384, Q buffers 0 / 32 KB), K/V stages rotating over 4 x 32 KB; per round and slot:
+// PV (8 TS into O_t, P = S_t cols), QK (8 SS into S_t), commits like the kernel.
+template <int MODE_SEQ>
+__global__ void __launch_bounds__(128, 1) k_attn_seq(long long* out, int iters) {
+  extern __shared__ __align__(1024) uint8_t sm[];
+  __shared__ uint64_t bar[4];
+  __shared__ uint32_t tslot;
+  const int warp = threadIdx.x >> 5;
+  if (threadIdx.x == 0) { for (int i = 0; i < 4; ++i) mbar_init(bar + i, 1); fence_barrier_init(); }
+  if (warp == 0) { tmem_alloc(&tslot, 512); tmem_relinquish(); }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = tslot;
+  if (threadIdx.x == 0) {
+    const uint32_t q0 = smem_u32(sm), kv = smem_u32(sm + 65536);
+    constexpr uint32_t idq = idesc_bf16_f32(128, 128, 0, 0);
+    constexpr uint32_t idp = idesc_bf16_f32(128, 128, 0, 1);
+    int st = 0;
+    const long long t0 = clock64();
+    for (int it = 0; it < iters; ++it) {
+      for (int t = 0; t < 2; ++t) {
+        const uint32_t vb = kv + (st & 3) * 32768u; ++st;
+        for (int kk = 0; kk < 8; ++kk)
+          mma_ts(tmem + 256 + t * 128, tmem + t * 128 + kk * 8, sdesc_sw128(vb + kk * 2048, 16384, 1024), idp, kk > 0 || it > 0);
+        mma_commit(bar + 0);
+        if (MODE_SEQ & 1) { mma_commit(bar + 1); mma_commit(bar + 2); }
+        const uint32_t kb = kv + (st & 3) * 32768u; ++st;
+        const uint32_t qb = q0 + t * 32768u;
+        for (int kk = 0; kk < 8; ++kk)
+          mma_ss(tmem + t * 128, sdesc_sw128(qb + (kk >> 2) * 16384 + (kk & 3) * 32, 16, 1024),
+                 sdesc_sw128(kb + (kk >> 2) * 16384 + (kk & 3) * 32, 16, 1024), idq, kk > 0);
+        mma_commit(bar + 1);
+        mma_commit(bar + 2 + t);
+      }
+    }
+    mma_commit(bar + 0);
+    out[blockIdx.x] = clock64() - t0;
   }
   tc_fence_before();
   __syncthreads();
@@ -137,9 +241,42 @@ int main() {
   run<64, false>("SS M128 N64", sms);
   run<128, true>("TS M128 N128 (PV)", sms);
   run<256, true>("TS M128 N256", sms);
+  for (int busy = 0; busy < 2; ++busy) {
+    long long* d; cudaMalloc(&d, sizeof(long long) * 512);
+    cudaFuncSetAttribute(k_ldtm_under_mma, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    k_ldtm_under_mma<<<sms, 160, 200 * 1024>>>(d, 2000, busy);
+    cudaError_t e = cudaDeviceSynchronize();
+    long long h[148]; cudaMemcpy(h, d, sizeof(long long) * sms, cudaMemcpyDeviceToHost);
+    double avg = 0; for (int i = 0; i < sms; ++i) avg += h[i]; avg /= sms;
+    printf("4 x LDTM.x32 + wait, tensor pipe %s: %.0f clk (%s)\n", busy ? "busy" : "idle", avg,
+           e == cudaSuccess ? "ok" : cudaGetErrorString(e));
+    cudaFree(d);
+  }
+  {
+    long long* d; cudaMalloc(&d, sizeof(long long) * 256);
+    cudaFuncSetAttribute(k_attn_seq<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(k_attn_seq<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    const int iters = 256;
+    k_attn_seq<1><<<sms, 128, 200 * 1024>>>(d, iters);
+    cudaDeviceSynchronize();
+    { long long h[148]; cudaMemcpy(h, d, sizeof(long long) * sms, cudaMemcpyDeviceToHost);
+      double avg = 0; for (int i = 0; i < sms; ++i) avg += h[i]; avg /= sms;
+      printf("attention MMA sequence, 3 commits after PV: %.1f clk per round (ideal 2048)\n", avg / iters); }
+    k_attn_seq<0><<<sms, 128, 200 * 1024>>>(d, iters);
+    cudaError_t e = cudaDeviceSynchronize();
+    long long h[148]; cudaMemcpy(h, d, sizeof(long long) * sms, cudaMemcpyDeviceToHost);
+    double avg = 0; for (int i = 0; i < sms; ++i) avg += h[i]; avg /= sms;
+    printf("attention MMA sequence (2 slots, no waits): %.1f clk per round of 32 MMAs (ideal 2048) %s\n",
+           avg / iters, e == cudaSuccess ? "ok" : cudaGetErrorString(e));
+    cudaFree(d);
+  }
   run_mix<0>("mix SS8+TS8", sms);
   run_mix<1>("mix + LDTM background", sms);
   run_mix<3>("mix + LDTM/STTM background", sms);
   run_mix<4>("mix, wait each iteration", sms);
+  run_mix<8>("mix + done-wait/fence per iteration", sms);
+  run_mix<32>("mix, B rotating over 4 stages", sms);
+  run_mix<64>("mix + 4 warps polling an mbarrier", sms);
+  run_mix<24>("mix + done-wait/fence x2 per iteration", sms);
   return 0;
 }

@@ -96,6 +96,16 @@ constexpr uint8_t EMPTY_TILE = 0xFF;
 // on ~grid consecutive items (a few heads, L2-resident K/V); CTA c takes position
 // (c + k*R) mod grid of window k so a CTA does not keep drawing the same query-tile index.
 constexpr int ORDER = SV_ORDER;
+#ifndef SV_MMA_POLL
+#define SV_MMA_POLL 0
+#endif
+// The MMA issuer polls its barriers (mbarrier.test_wait) instead of try_wait, which may
+// suspend the thread: a suspended issuer wakes late and leaves the tensor pipe idle.
+#if SV_MMA_POLL
+#define SV_MMA_WAIT mbar_wait_spin
+#else
+#define SV_MMA_WAIT mbar_wait
+#endif
 
 __host__ __device__ inline int gcd_int(int a, int b) {
   while (b) { const int t = a % b; a = b; b = t; }
@@ -536,7 +546,7 @@ attn_fwd_kernel(const __grid_constant__ CUtensorMap tmap_q,
           const int s = kv_idx % C::NST;
           const uint32_t ph = (kv_idx / C::NST) & 1;
           ++kv_idx;
-          mbar_wait(kv_full + s, ph);
+          SV_MMA_WAIT(kv_full + s, ph);
           return (uint32_t)s;
         };
         auto issue_qk = [&](int t, uint32_t s, int qb, bool last) {
@@ -566,7 +576,7 @@ attn_fwd_kernel(const __grid_constant__ CUtensorMap tmap_q,
           const int n = sm->n[ic];
           if (t) { qb1 = qb; nn1 = n; jn1 = 0; } else { qb0 = qb; nn0 = n; jn0 = 0; }
           const uint32_t s = next_stage();
-          mbar_wait(q_full + qb, (meta >> 3) & 1);
+          SV_MMA_WAIT(q_full + qb, (meta >> 3) & 1);
           tc_fence_after();
           issue_qk(t, s, qb, n == 1);
         };
@@ -589,9 +599,9 @@ attn_fwd_kernel(const __grid_constant__ CUtensorMap tmap_q,
             const uint32_t o_tmem = tmem + 256 + t * D;
             const uint32_t p_tmem = tmem + t * 128;
             // the tile's first P.V overwrites O: the epilogue must have drained the previous one
-            if (jn == 0 && tdone > 0) mbar_wait(o_free + t, (tdone - 1) & 1);
+            if (jn == 0 && tdone > 0) SV_MMA_WAIT(o_free + t, (tdone - 1) & 1);
             // O_t += P_t V_j in two halves: the first as soon as half of P is in TMEM
-            mbar_wait(p_bar + 2 * t, par);
+            SV_MMA_WAIT(p_bar + 2 * t, par);
             tc_fence_after();
             if (leader) {
 #pragma unroll
@@ -600,7 +610,7 @@ attn_fwd_kernel(const __grid_constant__ CUtensorMap tmap_q,
                        (jn > 0 || kk > 0) ? 1u : 0u);
             }
             __syncwarp();
-            mbar_wait(p_bar + 2 * t + 1, par);
+            SV_MMA_WAIT(p_bar + 2 * t + 1, par);
             tc_fence_after();
             if (leader) {
 #pragma unroll

@@ -59,3 +59,12 @@ print("  MMA total %.0f: wait P %.0f (%.0f%%)  wait KV %.0f (%.0f%%)  wait O-fre
     100 * np.median(kw / np.maximum(mt, 1)), np.median(ow), np.median(qw)))
 lt, lw = cta(6400), cta(6600)
 print("  KV loader total %.0f: wait empty stage %.0f (%.0f%%)" % (np.median(lt), np.median(lw), 100 * np.median(lw / np.maximum(lt, 1))))
+
+tr = a[2048:2048 + 5 * 400].reshape(-1, 5)
+tr = tr[tr[:, 0] > 0]
+if len(tr) > 20:
+    # v3 MMA warp per step: [t0 before V stage wait, t1 after, t2 after P wait, t3 after PV issue, t4 after QK(g+2) issue]
+    d = np.diff(tr, axis=1)
+    print("MMA step trace (CTA0) medians clk: V-stage wait %.0f | P wait %.0f | PV issue %.0f | QK issue %.0f | gap %.0f | period %.0f" % (
+        np.median(d[:, 0]), np.median(d[:, 1]), np.median(d[:, 2]), np.median(d[:, 3]),
+        np.median(tr[1:, 0] - tr[:-1, 4]), np.median(np.diff(tr[:, 0]))))
