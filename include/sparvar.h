@@ -161,6 +161,36 @@ sparvar_status sparvar_dense_attn(const sparvar_schedule* sched, int32_t target_
                                   const uint16_t* k_cache, const uint16_t* v_cache,
                                   float softmax_scale, uint16_t* o, float* lse, void* stream);
 
+/* NEXT(1) — CS4A dense-attention cache residual at the decision scale S:
+ *   O_cache = O_dense - Softmax(Q_S K_inds^T) V_inds, the sparse term being the block-sparse
+ *   attention over the decision-scale lists (row_ptr_S / col_idx_S, e.g. built from the
+ *   predictor's mask with sparvar_build_block_lists).  Runs the dense kernel into o_cache, the
+ *   block-sparse kernel into o_scratch, then subtracts in fp32 (bf16 result).
+ *   q_S: bf16 [BH][N_S][D]; o_scratch, o_cache: caller-owned bf16 [BH][N_S][D] with the shape's
+ *   o_stride_bh, must not alias.  block as for sparvar_block_sparse_attn.
+ */
+sparvar_status sparvar_cache_residual(const sparvar_schedule* sched, int32_t decision_scale,
+                                     int32_t block, const sparvar_attn_shape* shape,
+                                     const uint16_t* q_S, const uint16_t* k_cache,
+                                     const uint16_t* v_cache, const int32_t* row_ptr_S,
+                                     const int32_t* col_idx_S, float softmax_scale,
+                                     uint16_t* o_scratch, uint16_t* o_cache, void* stream);
+
+/* NEXT(1) — cached block-sparse attention at scale K:
+ *   O^(K) = Upsample(O_cache) + Delta O^(K), Delta O^(K) = sparvar_block_sparse_attn output.
+ *   Upsample is nearest neighbour over the query grid: output query (x, y) of side s_K adds
+ *   cache row (floor(x s_S / s_K), floor(y s_S / s_K)) of side s_S = side of cache_scale
+ *   (READING 22).  The addition is fused into the attention epilogue (fp32, bf16 result); rows
+ *   with an empty list get the cache row alone.  lse (nullable) is that of Delta O.
+ *   o_cache: bf16 [BH][N_S][D] with cache_stride_bh elements between (b,h) slabs.
+ */
+sparvar_status sparvar_block_sparse_attn_cached(
+    const sparvar_schedule* sched, int32_t target_scale, int32_t block,
+    const sparvar_attn_shape* shape, const uint16_t* q, const uint16_t* k_cache,
+    const uint16_t* v_cache, const int32_t* row_ptr, const int32_t* col_idx, float softmax_scale,
+    const uint16_t* o_cache, int32_t cache_scale, int64_t cache_stride_bh, uint16_t* o, float* lse,
+    void* stream);
+
 /* Thread-local message for the last non-OK status of this thread ("" if none). */
 const char* sparvar_last_error(void);
 

@@ -21,7 +21,8 @@ import torch
 
 __all__ = [
     "lib", "SparVARError", "geometry", "local_mask", "predict_pattern", "map_indices",
-    "build_block_lists", "block_sparse_attn", "dense_attn", "SparseLayer", "unpack_bits",
+    "build_block_lists", "block_sparse_attn", "dense_attn", "cache_residual",
+    "block_sparse_attn_cached", "SparseLayer", "unpack_bits",
     "SELECT_TOPK", "SELECT_THRESHOLD", "MAP_FOOTPRINT", "MAP_POINT",
 ]
 
@@ -64,6 +65,9 @@ def _load(path: str = LIB_PATH):
         "sparvar_build_block_lists": [I32, I32, I32, P, P, I32, P, P, I64, P, P],
         "sparvar_block_sparse_attn": [S, I32, I32, SH, P, P, P, P, P, F32, P, P, P],
         "sparvar_dense_attn": [S, I32, SH, P, P, P, F32, P, P, P],
+        "sparvar_cache_residual": [S, I32, I32, SH, P, P, P, P, P, F32, P, P, P],
+        "sparvar_block_sparse_attn_cached": [S, I32, I32, SH, P, P, P, P, P, F32, P, I32, I64, P,
+                                             P, P],
     }
     for name, args in sig.items():
         f = getattr(L, name)
@@ -215,6 +219,43 @@ def dense_attn(sides, target: int, q, k_cache, v_cache, softmax_scale: float = 0
     _check(lib.sparvar_dense_attn(ctypes.byref(_sched(sides)), target, ctypes.byref(sh), _ptr(q),
                                   _ptr(k_cache), _ptr(v_cache), softmax_scale, _ptr(o), _ptr(lse),
                                   _stream(stream)))
+    return o
+
+
+def cache_residual(sides, decision_scale: int, block: int, q_S, k_cache, v_cache, row_ptr_S,
+                   col_idx_S, softmax_scale: float = 0.0, o_cache=None, o_scratch=None,
+                   stream=None):
+    """NEXT(1): O_cache = O_dense - O_sparse at the decision scale."""
+    if o_cache is None:
+        o_cache = torch.empty_like(q_S)
+    if o_scratch is None:
+        o_scratch = torch.empty_like(q_S)
+    if _bh_view(v_cache, "v_cache") != k_cache.stride(0):
+        raise ValueError("k_cache and v_cache must share a (b,h) stride")
+    if o_scratch.stride(0) != o_cache.stride(0):
+        raise ValueError("o_scratch and o_cache must share a (b,h) stride")
+    sh = _attn_shape(q_S, k_cache, o_cache)
+    _check(lib.sparvar_cache_residual(ctypes.byref(_sched(sides)), decision_scale, block,
+                                      ctypes.byref(sh), _ptr(q_S), _ptr(k_cache), _ptr(v_cache),
+                                      _ptr(row_ptr_S), _ptr(col_idx_S), softmax_scale,
+                                      _ptr(o_scratch), _ptr(o_cache), _stream(stream)))
+    return o_cache
+
+
+def block_sparse_attn_cached(sides, target: int, block: int, q, k_cache, v_cache, row_ptr,
+                             col_idx, o_cache, cache_scale: int, softmax_scale: float = 0.0,
+                             o=None, lse=None, stream=None):
+    """NEXT(1): O^(K) = NN-upsample(O_cache) + Delta O^(K), fused epilogue."""
+    if o is None:
+        o = torch.empty_like(q)
+    if _bh_view(v_cache, "v_cache") != k_cache.stride(0):
+        raise ValueError("k_cache and v_cache must share a (b,h) stride")
+    cstride = _bh_view(o_cache, "o_cache")
+    sh = _attn_shape(q, k_cache, o)
+    _check(lib.sparvar_block_sparse_attn_cached(
+        ctypes.byref(_sched(sides)), target, block, ctypes.byref(sh), _ptr(q), _ptr(k_cache),
+        _ptr(v_cache), _ptr(row_ptr), _ptr(col_idx), softmax_scale, _ptr(o_cache), cache_scale,
+        cstride, _ptr(o), _ptr(lse), _stream(stream)))
     return o
 
 

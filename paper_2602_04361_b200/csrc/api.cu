@@ -263,7 +263,9 @@ static sparvar_status attn_common(const sparvar_schedule* sched, int32_t target_
                                   int32_t block, const sparvar_attn_shape* shape,
                                   const uint16_t* q, const uint16_t* k, const uint16_t* v,
                                   const int32_t* row_ptr, const int32_t* col_idx, float scale_in,
-                                  uint16_t* o, float* lse, void* stream) {
+                                  uint16_t* o, float* lse, void* stream,
+                                  const uint16_t* add = nullptr, int32_t add_scale = 0,
+                                  int64_t add_stride = 0) {
   sv::Geo g;
   sparvar_status s = make_geo(sched, &g);
   if (s != SPARVAR_OK) return s;
@@ -292,6 +294,10 @@ static sparvar_status attn_common(const sparvar_schedule* sched, int32_t target_
   a.o = o;
   a.o_stride = shape->o_stride_bh;
   a.lse = lse;
+  a.add = add;
+  a.add_stride = add_stride;
+  a.s_dst = g.side[target_scale - 1];
+  a.s_src = add != nullptr ? g.side[add_scale - 1] : 1;
   CUtensorMap tq, tk, tv;
   if ((s = make_tmap(&tq, q, D, n_q, a.bh, shape->q_stride_bh, 128)) != SPARVAR_OK) return s;
   if ((s = make_tmap(&tk, k, D, n_kv, a.bh, shape->kv_stride_bh, block)) != SPARVAR_OK) return s;
@@ -313,12 +319,55 @@ sparvar_status sparvar_block_sparse_attn(const sparvar_schedule* sched, int32_t 
                      softmax_scale, o, lse, stream);
 }
 
+sparvar_status sparvar_cache_residual(const sparvar_schedule* sched, int32_t decision_scale,
+                                     int32_t block, const sparvar_attn_shape* shape,
+                                     const uint16_t* q_S, const uint16_t* k_cache,
+                                     const uint16_t* v_cache, const int32_t* row_ptr_S,
+                                     const int32_t* col_idx_S, float softmax_scale,
+                                     uint16_t* o_scratch, uint16_t* o_cache, void* stream) {
+  if (row_ptr_S == nullptr || col_idx_S == nullptr || o_scratch == nullptr || o_cache == nullptr)
+    return fail(SPARVAR_ERR_INVALID_ARG, "null row_ptr / col_idx / output pointer");
+  if (o_scratch == o_cache) return fail(SPARVAR_ERR_INVALID_ARG, "o_scratch must not alias o_cache");
+  sparvar_status s = attn_common(sched, decision_scale, 128, shape, q_S, k_cache, v_cache, nullptr,
+                                 nullptr, softmax_scale, o_cache, nullptr, stream);
+  if (s != SPARVAR_OK) return s;
+  s = attn_common(sched, decision_scale, block, shape, q_S, k_cache, v_cache, row_ptr_S, col_idx_S,
+                  softmax_scale, o_scratch, nullptr, stream);
+  if (s != SPARVAR_OK) return s;
+  const int side = sched->sides[decision_scale - 1];
+  cudaError_t e = sv::launch_residual(shape->batch_heads, side * side, shape->head_dim, o_cache,
+                                      shape->o_stride_bh, o_scratch, shape->o_stride_bh, o_cache,
+                                      shape->o_stride_bh, (cudaStream_t)stream);
+  if (e != cudaSuccess) return cuda_fail(e, "residual launch");
+  return ok();
+}
+
+sparvar_status sparvar_block_sparse_attn_cached(
+    const sparvar_schedule* sched, int32_t target_scale, int32_t block,
+    const sparvar_attn_shape* shape, const uint16_t* q, const uint16_t* k_cache,
+    const uint16_t* v_cache, const int32_t* row_ptr, const int32_t* col_idx, float softmax_scale,
+    const uint16_t* o_cache, int32_t cache_scale, int64_t cache_stride_bh, uint16_t* o, float* lse,
+    void* stream) {
+  if (row_ptr == nullptr || col_idx == nullptr || o_cache == nullptr)
+    return fail(SPARVAR_ERR_INVALID_ARG, "null row_ptr / col_idx / o_cache");
+  if (sched == nullptr || cache_scale < 1 || cache_scale > target_scale ||
+      cache_scale > sched->num_scales)
+    return fail(SPARVAR_ERR_INVALID_ARG, "cache_scale %d not in [1, target_scale]", cache_scale);
+  if (shape == nullptr) return fail(SPARVAR_ERR_INVALID_ARG, "null shape");
+  const long long n_S = (long long)sched->sides[cache_scale - 1] * sched->sides[cache_scale - 1];
+  if (cache_stride_bh < n_S * shape->head_dim || cache_stride_bh % 8 != 0 || !aligned16(o_cache))
+    return fail(SPARVAR_ERR_INVALID_ARG, "cache_stride_bh must be >= N_S*D, a multiple of 8, "
+                "and o_cache 16-byte aligned");
+  return attn_common(sched, target_scale, block, shape, q, k_cache, v_cache, row_ptr, col_idx,
+                     softmax_scale, o, lse, stream, o_cache, cache_scale, cache_stride_bh);
+}
+
 sparvar_status sparvar_dense_attn(const sparvar_schedule* sched, int32_t target_scale,
                                   const sparvar_attn_shape* shape, const uint16_t* q,
                                   const uint16_t* k_cache, const uint16_t* v_cache,
                                   float softmax_scale, uint16_t* o, float* lse, void* stream) {
   return attn_common(sched, target_scale, 128, shape, q, k_cache, v_cache, nullptr, nullptr,
-                     softmax_scale, o, lse, stream);
+                     softmax_scale, o, lse, stream, nullptr, 0, 0);
 }
 
 }  // extern "C"

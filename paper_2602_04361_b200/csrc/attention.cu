@@ -200,6 +200,32 @@ struct Steps {
   }
 };
 
+// NEXT(1): source row of the nearest-neighbour upsampled cache residual for output query
+// n_row of scale K: (x, y) = divmod(n_row, s_K) -> (floor(x s_S / s_K), floor(y s_S / s_K))
+// (READING 22); nullptr when no residual is fused.
+template <int D>
+__device__ __forceinline__ const uint16_t* cache_row(const AttnArgs& a, int bh, int n_row) {
+  if (a.add == nullptr) return nullptr;
+  const int x = n_row / a.s_dst, y = n_row % a.s_dst;
+  const int src = (x * a.s_src / a.s_dst) * a.s_src + (y * a.s_src / a.s_dst);
+  return a.add + (long long)bh * a.add_stride + (long long)src * D;
+}
+__device__ __forceinline__ void load_cache16(const uint16_t* p, float* out) {
+  if (p == nullptr) {
+#pragma unroll
+    for (int i = 0; i < 16; ++i) out[i] = 0.f;
+    return;
+  }
+  const uint4 u0 = *reinterpret_cast<const uint4*>(p);
+  const uint4 u1 = *reinterpret_cast<const uint4*>(p + 8);
+  const uint32_t w[8] = {u0.x, u0.y, u0.z, u0.w, u1.x, u1.y, u1.z, u1.w};
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    out[2 * i] = __uint_as_float(w[i] << 16);
+    out[2 * i + 1] = __uint_as_float(w[i] & 0xffff0000u);
+  }
+}
+
 // Cost prefix F(i) of the first i items of [item_begin, item_end) (monotone in i): listed blocks
 // (row_ptr prefix sums) + TILE_OVERHEAD per tile.
 template <int G>
@@ -424,6 +450,7 @@ attn_fwd_kernel(const __grid_constant__ CUtensorMap tmap_q,
         const int n_row = tile * BM + row;
         const bool store = n_row < a.n_q;
         uint16_t* orow = a.o + (long long)bh * a.o_stride + (long long)n_row * D;
+        const uint16_t* arow = cache_row<D>(a, bh, n_row);
 #pragma unroll 1
         for (int c = 0; c < D; c += 16) {
           uint32_t o[16];
@@ -433,10 +460,13 @@ attn_fwd_kernel(const __grid_constant__ CUtensorMap tmap_q,
             tc_fence_before();
             mbar_arrive(o_free + t);      // O of this slot may be overwritten now
           }
+          float add[16];
+          load_cache16(arow != nullptr && store ? arow + c : nullptr, add);
           uint32_t pk[8];
 #pragma unroll
           for (int q = 0; q < 8; ++q)
-            pk[q] = pack_bf16x2(__uint_as_float(o[2 * q]) * stt.x, __uint_as_float(o[2 * q + 1]) * stt.x);
+            pk[q] = pack_bf16x2(fmaf(__uint_as_float(o[2 * q]), stt.x, add[2 * q]),
+                                fmaf(__uint_as_float(o[2 * q + 1]), stt.x, add[2 * q + 1]));
           if (store) {
             uint4* dst = reinterpret_cast<uint4*>(orow + c);
             dst[0] = make_uint4(pk[0], pk[1], pk[2], pk[3]);
@@ -526,7 +556,10 @@ attn_fwd_kernel(const __grid_constant__ CUtensorMap tmap_q,
             if (row >= a.n_q) continue;
             uint4* dst =
                 reinterpret_cast<uint4*>(a.o + (long long)bh * a.o_stride + (long long)row * D);
-            for (int c = 0; c < D / 8; ++c) dst[c] = make_uint4(0, 0, 0, 0);
+            // empty sparse part: the output is the (upsampled) cache residual, if any
+            const uint16_t* arow = cache_row<D>(a, bh, row);
+            for (int c = 0; c < D / 8; ++c)
+              dst[c] = arow != nullptr ? reinterpret_cast<const uint4*>(arow)[c] : make_uint4(0, 0, 0, 0);
             if (a.lse != nullptr) a.lse[(long long)bh * a.n_q + row] = -INFINITY;
           }
         }
@@ -841,7 +874,42 @@ cudaError_t launch_t(const CUtensorMap& tq, const CUtensorMap& tk, const CUtenso
   return cudaGetLastError();
 }
 
+// o_cache = o_dense - o_sparse (NEXT(1)): bf16 in, fp32 difference, bf16 out;
+// 8 elements (16 B) per thread per iteration, grid-stride over all (b,h) rows.
+__global__ void __launch_bounds__(256) residual_kernel(int bh, int rows, int D, const uint16_t* dense,
+                                                       long long ds, const uint16_t* sparse,
+                                                       long long ss, uint16_t* out, long long os) {
+  const long long per_bh = (long long)rows * D / 8;
+  const long long total = per_bh * bh;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
+       i += (long long)gridDim.x * blockDim.x) {
+    const long long b = i / per_bh, e = (i % per_bh) * 8;
+    const uint4 x = *reinterpret_cast<const uint4*>(dense + b * ds + e);
+    const uint4 y = *reinterpret_cast<const uint4*>(sparse + b * ss + e);
+    const uint32_t xs[4] = {x.x, x.y, x.z, x.w}, ys[4] = {y.x, y.y, y.z, y.w};
+    uint32_t r[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const float lo = __uint_as_float(xs[k] << 16) - __uint_as_float(ys[k] << 16);
+      const float hi = __uint_as_float(xs[k] & 0xffff0000u) - __uint_as_float(ys[k] & 0xffff0000u);
+      r[k] = pack_bf16x2(lo, hi);
+    }
+    *reinterpret_cast<uint4*>(out + b * os + e) = make_uint4(r[0], r[1], r[2], r[3]);
+  }
+}
+
 }  // namespace
+
+cudaError_t launch_residual(int bh, int rows, int D, const uint16_t* dense, long long dense_stride,
+                            const uint16_t* sparse, long long sparse_stride, uint16_t* out,
+                            long long out_stride, cudaStream_t st) {
+  const long long vec = (long long)bh * rows * D / 8;
+  if (vec <= 0) return cudaSuccess;
+  const int grid = (int)((vec + 255) / 256 < 4L * num_sms() ? (vec + 255) / 256 : 4L * num_sms());
+  residual_kernel<<<grid, 256, 0, st>>>(bh, rows, D, dense, dense_stride, sparse, sparse_stride,
+                                        out, out_stride);
+  return cudaGetLastError();
+}
 
 cudaError_t launch_attention(int head_dim, int block, const CUtensorMap& tq, const CUtensorMap& tk,
                              const CUtensorMap& tv, const AttnArgs& a, cudaStream_t st) {

@@ -42,7 +42,15 @@ struct AttnArgs {
   uint16_t* o;
   long long o_stride; // elements between (b,h) slabs of O
   float* lse;
+  // optional NEXT(1) cache residual added in the epilogue: o += NN-upsample(add) (READING 22)
+  const uint16_t* add;   // bf16 [bh][s_src*s_src][D] or nullptr
+  long long add_stride;  // elements between (b,h) slabs of add
+  int s_src, s_dst;      // query grid sides of the cache (S) and of the output (K)
 };
+// o_cache = o_dense - o_sparse, bf16 in / out, fp32 arithmetic (NEXT(1))
+cudaError_t launch_residual(int bh, int rows, int D, const uint16_t* dense, long long dense_stride,
+                            const uint16_t* sparse, long long sparse_stride, uint16_t* out,
+                            long long out_stride, cudaStream_t st);
 cudaError_t launch_attention(int head_dim, int block, const CUtensorMap& tq, const CUtensorMap& tk,
                              const CUtensorMap& tv, const AttnArgs& a, cudaStream_t st);
 

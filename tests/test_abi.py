@@ -25,7 +25,7 @@ def _declared():
 
 def test_exports_every_declared_symbol(sv):
     names = _declared()
-    assert "sparvar_block_sparse_attn" in names and len(names) == 8
+    assert "sparvar_block_sparse_attn" in names and len(names) == 10
     L = ctypes.CDLL(sv.LIB_PATH)
     for n in names:
         assert hasattr(L, n), n

@@ -1,0 +1,92 @@
+"""GPU parity of NEXT(1), the CS4A cache residual, through the C ABI against
+the fp64 oracle (oracle/cache.py) on the same bf16 inputs: max |diff| <= 1e-2, mean <= 1e-3."""
+import numpy as np
+import pytest
+import torch
+
+from oracle.attention import merge_lists
+from oracle.cache import cache_residual, cached_sparse
+from oracle.geometry import INFINITY_1K_SIDES, Schedule, ceil_div
+from oracle.mapping import map_pattern
+from synth import kv_cache_iid, q_iid
+from tests.helpers import EQ256, MAX_ABS, MEAN_ABS, attn_errors, bits_to_bool, to_np
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def sv():
+    import paper_2602_04361_b200 as m
+    return m
+
+
+def _case(sv, sides, S, K, B, D, bh, sink, topk, seed):
+    sched = Schedule(sides)
+    qS = q_iid(seed, S, 0, bh, sched.N(S), D).cuda()
+    qK = q_iid(seed, K, 0, bh, sched.N(K), D).cuda()
+    k, v = kv_cache_iid(seed, 0, bh, sched.C(K), D)
+    k, v = k.cuda(), v.cuda()
+    gS, gK = sv.geometry(sides, S, B), sv.geometry(sides, K, B)
+    src, _ = sv.predict_pattern(sides, S, B, sink, qS, k, sv.SELECT_TOPK, topk)
+    rpS, ciS, stS = sv.build_block_lists(bh, gS["G_q"], gS["G_kv"], [(src, False)])
+    dst = sv.map_indices(sides, S, K, B, sink, src)
+    rpK, ciK, stK = sv.build_block_lists(bh, gK["G_q"], gK["G_kv"], [(dst, False)])
+    oc = sv.cache_residual(sides, S, B, qS, k, v, rpS, ciS)
+    o = sv.block_sparse_attn_cached(sides, K, B, qK, k, v, rpK, ciK, oc, S)
+    torch.cuda.synchronize()
+    assert stS.item() == 0 and stK.item() == 0
+    src_b = bits_to_bool(src.cpu().numpy(), gS["G_kv"])
+    return sched, qS, qK, k, v, src_b, oc, o
+
+
+@pytest.mark.parametrize("cfg", [EQ256], ids=["256eq"])
+def test_cache_residual_and_cached_attention(sv, cfg):
+    sides, S, K, B, D = cfg["sides"], cfg["S"], cfg["K"], cfg["B"], cfg["D"]
+    bh, sink = 3, cfg["sink"]
+    sched, qS, qK, k, v, src_b, oc, o = _case(sv, sides, S, K, B, D, bh, sink, 2, 9)
+    for b in range(bh):
+        lists_S = merge_lists([src_b[b]])
+        want_oc = cache_residual(to_np(qS[b]), to_np(k[b]), to_np(v[b]), sched.C(S), B, lists_S)
+        mx, mean = attn_errors(to_np(oc[b]), want_oc)
+        assert mx <= MAX_ABS and mean <= MEAN_ABS, ("o_cache", mx, mean)
+        lists_K = merge_lists([map_pattern(src_b[b], sched, S, K, B, sink, "footprint")])
+        want = cached_sparse(to_np(qK[b]), to_np(k[b]), to_np(v[b]), sched.C(K), B, lists_K,
+                             want_oc, sides[S - 1], sides[K - 1])
+        mx, mean = attn_errors(to_np(o[b]), want)
+        assert mx <= MAX_ABS and mean <= MEAN_ABS, ("O^(K)", mx, mean)
+
+
+def test_full_size_sampled(sv):
+    """Infinity-1K, S=11 -> K=13, B=128: sampled query blocks of the cached output."""
+    sides, S, K, B, D, bh, sink = list(INFINITY_1K_SIDES), 11, 13, 128, 128, 2, 5
+    sched, qS, qK, k, v, src_b, oc, o = _case(sv, sides, S, K, B, D, bh, sink, 5, 10)
+    gq = ceil_div(sched.N(K), B)
+    for b in range(bh):
+        lists_S = merge_lists([src_b[b]])
+        want_oc = cache_residual(to_np(qS[b]), to_np(k[b]), to_np(v[b]), sched.C(S), B, lists_S)
+        lists_K = merge_lists([map_pattern(src_b[b], sched, S, K, B, sink, "footprint")])
+        rows_u = [0, 7, gq - 1]
+        from oracle.attention import block_sparse
+        from oracle.cache import upsample_nn
+        delta = block_sparse(to_np(qK[b]), to_np(k[b]), to_np(v[b]), sched.C(K), B, lists_K,
+                             rows=rows_u)
+        want = delta + upsample_nn(want_oc, sides[S - 1], sides[K - 1])
+        sel = np.concatenate([np.arange(u * B, (u + 1) * B) for u in rows_u])
+        mx, mean = attn_errors(to_np(o[b])[sel], want[sel])
+        assert mx <= MAX_ABS and mean <= MEAN_ABS, (mx, mean)
+
+
+def test_all_blocks_cache_is_zero(sv):
+    sides, S, B, D, bh = [1, 2, 4, 6, 8], 5, 32, 64, 2
+    sched = Schedule(sides)
+    qS = q_iid(11, S, 0, bh, sched.N(S), D).cuda()
+    k, v = kv_cache_iid(11, 0, bh, sched.C(S), D)
+    k, v = k.cuda(), v.cuda()
+    gq, gkv = ceil_div(sched.N(S), B), ceil_div(sched.C(S), B)
+    from tests.helpers import bool_to_bits
+    m = torch.from_numpy(bool_to_bits(np.ones((bh, gq, gkv), dtype=bool))).cuda()
+    rp, ci, st = sv.build_block_lists(bh, gq, gkv, [(m, False)])
+    oc = sv.cache_residual(sides, S, B, qS, k, v, rp, ci)
+    torch.cuda.synchronize()
+    # dense (B=128 tiles) and all-blocks sparse (B=32) agree to bf16 rounding of the outputs
+    assert oc.float().abs().max().item() <= 2e-3
