@@ -88,5 +88,8 @@ def test_all_blocks_cache_is_zero(sv):
     rp, ci, st = sv.build_block_lists(bh, gq, gkv, [(m, False)])
     oc = sv.cache_residual(sides, S, B, qS, k, v, rp, ci)
     torch.cuda.synchronize()
-    # dense (B=128 tiles) and all-blocks sparse (B=32) agree to bf16 rounding of the outputs
-    assert oc.float().abs().max().item() <= 2e-3
+    # the oracle's cache is exactly 0 here (tests/test_oracle_cache.py); the GPU's is the
+    # difference of two bf16 attention outputs whose P was rounded to bf16 against different
+    # running maxima, so it is held to the north-star attention tolerance against that 0
+    mx, mean = attn_errors(to_np(oc.reshape(-1, D)), np.zeros((oc.numel() // D, D)))
+    assert mx <= MAX_ABS and mean <= MEAN_ABS, (mx, mean)
