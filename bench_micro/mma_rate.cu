@@ -202,6 +202,39 @@ __global__ void __launch_bounds__(128, 1) k_attn_seq(long long* out, int iters) 
   if (warp == 0) { tc_fence_after(); tmem_dealloc(tmem, 512); }
 }
 
+// tcgen05.mma issue queue depth: time each issue return of 24 back-to-back MMAs on an idle pipe
+__global__ void __launch_bounds__(32, 1) k_qdepth(long long* out) {
+  extern __shared__ __align__(1024) uint8_t sm[];
+  __shared__ uint32_t tslot;
+  __shared__ uint64_t bar;
+  if (threadIdx.x == 0) { mbar_init(&bar, 1); fence_barrier_init(); }
+  tmem_alloc(&tslot, 512);
+  tmem_relinquish();
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (threadIdx.x == 0) {
+    const uint32_t a = smem_u32(sm), b = smem_u32(sm + 32768);
+    constexpr uint32_t idq = idesc_bf16_f32(128, 128, 0, 0);
+    long long t[25];
+    const uint64_t da = sdesc_sw128(a, 16, 1024), db = sdesc_sw128(b, 16, 1024);
+    t[0] = clock64();
+#pragma unroll
+    for (int i = 0; i < 24; ++i) {
+      mma_ss(tslot, da + (i & 3) * 2, db + (i & 3) * 2, idq, 1);
+      t[i + 1] = clock64();
+    }
+    mma_commit(&bar);
+    mbar_wait(&bar, 0);
+    const long long te = clock64();
+    for (int i = 0; i < 25; ++i) out[i] = t[i] - t[0];
+    out[25] = te - t[0];
+  }
+  __syncwarp();
+  tc_fence_after();
+  if (threadIdx.x < 32) tmem_dealloc(tslot, 512);
+}
+
 template <int MODE>
 void run_mix(const char* name, int sms) {
   const int iters = 256;
@@ -241,6 +274,17 @@ int main() {
   run<64, false>("SS M128 N64", sms);
   run<128, true>("TS M128 N128 (PV)", sms);
   run<256, true>("TS M128 N256", sms);
+  {
+    long long* d; cudaMalloc(&d, sizeof(long long) * 32);
+    cudaFuncSetAttribute(k_qdepth, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
+    k_qdepth<<<1, 32, 100 * 1024>>>(d);
+    cudaDeviceSynchronize();
+    long long h[26]; cudaMemcpy(h, d, sizeof(h), cudaMemcpyDeviceToHost);
+    printf("issue-return times of 24 back-to-back MMAs (clk):");
+    for (int i = 1; i < 25; ++i) printf(" %lld", h[i]);
+    printf("  | all complete at %lld\n", h[25]);
+    cudaFree(d);
+  }
   for (int busy = 0; busy < 2; ++busy) {
     long long* d; cudaMalloc(&d, sizeof(long long) * 512);
     cudaFuncSetAttribute(k_ldtm_under_mma, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);

@@ -96,6 +96,9 @@ constexpr uint8_t EMPTY_TILE = 0xFF;
 // on ~grid consecutive items (a few heads, L2-resident K/V); CTA c takes position
 // (c + k*R) mod grid of window k so a CTA does not keep drawing the same query-tile index.
 constexpr int ORDER = SV_ORDER;
+#ifndef SV_LEAN
+#define SV_LEAN 1      // lean MMA issue loop (one P wait per op, no warp syncs)
+#endif
 #ifndef SV_MMA_POLL
 #define SV_MMA_POLL 0
 #endif
@@ -103,6 +106,8 @@ constexpr int ORDER = SV_ORDER;
 // suspend the thread: a suspended issuer wakes late and leaves the tensor pipe idle.
 #if SV_MMA_POLL
 #define SV_MMA_WAIT mbar_wait_spin
+#elif SV_MMA_DBG
+#define SV_MMA_WAIT(bar_, par_) mma_wait_dbg((bar_), (par_), kv_idx, (int)p_cnt0, (int)p_cnt1, jn0, jn1, icur0, icur1, __LINE__)
 #else
 #define SV_MMA_WAIT mbar_wait
 #endif
@@ -223,6 +228,21 @@ __device__ __forceinline__ void load_cache16(const uint16_t* p, float* out) {
   for (int i = 0; i < 8; ++i) {
     out[2 * i] = __uint_as_float(w[i] << 16);
     out[2 * i + 1] = __uint_as_float(w[i] & 0xffff0000u);
+  }
+}
+
+__device__ __forceinline__ void mma_wait_dbg(uint64_t* bar, uint32_t par, int kv, int p0, int p1,
+                                             int j0, int j1, int i0, int i1, int line) {
+  const uint32_t a = smem_u32(bar);
+  if (mbar_try_wait(a, par)) return;
+  const uint64_t t0 = globaltimer_ns();
+  bool said = false;
+  while (!mbar_try_wait(a, par)) {
+    if (!said && globaltimer_ns() - t0 > 1000000000ull) {
+      said = true;
+      if ((threadIdx.x & 31) == 0) printf("MMA stuck: block %d lane %d line %d bar 0x%x par %u kv_idx %d p_cnt %d %d jn %d %d icur %d %d\n",
+             blockIdx.x, threadIdx.x & 31, line, a, par, kv, p0, p1, j0, j1, i0, i1);
+    }
   }
 }
 
@@ -475,7 +495,6 @@ attn_fwd_kernel(const __grid_constant__ CUtensorMap tmap_q,
         }
         if (a.lse != nullptr && store) a.lse[(long long)bh * a.n_q + n_row] = stt.y;
       }
-      reg_alloc<REG_LAUNCH>();
     } else if (warp >= 8) {
       reg_dealloc<REG_PRODUCER>();
       if (warp == WARP_KV) {
@@ -575,11 +594,14 @@ attn_fwd_kernel(const __grid_constant__ CUtensorMap tmap_q,
         const uint64_t dk0 = sdesc_sw128(smem_u32(sKV), 16, 1024);
         const uint64_t dv0 = sdesc_sw128(smem_u32(sKV), BLK * 128, 1024);
         int icur0 = -1, icur1 = -1, jn0 = 0, jn1 = 0, nn0 = 0, nn1 = 0, qb0 = 0, qb1 = 0;
+        // ring position as (stage, phase) counters: no div/mod on the issue path
+        int ring_s = kv_idx % C::NST;
+        uint32_t ring_ph = (kv_idx / C::NST) & 1;
         auto next_stage = [&]() -> uint32_t {
-          const int s = kv_idx % C::NST;
-          const uint32_t ph = (kv_idx / C::NST) & 1;
+          const int s = ring_s;
+          SV_MMA_WAIT(kv_full + s, ring_ph);
+          if (++ring_s == C::NST) { ring_s = 0; ring_ph ^= 1; }
           ++kv_idx;
-          SV_MMA_WAIT(kv_full + s, ph);
           return (uint32_t)s;
         };
         auto issue_qk = [&](int t, uint32_t s, int qb, bool last) {
@@ -596,7 +618,9 @@ attn_fwd_kernel(const __grid_constant__ CUtensorMap tmap_q,
             mma_commit(s_bar + t);
             if (last) mma_commit(q_empty + qb);   // last use of this Q buffer
           }
+#if !SV_LEAN
           __syncwarp();
+#endif
         };
         auto start = [&](int t, int from) {
           int i = from;
@@ -633,6 +657,20 @@ attn_fwd_kernel(const __grid_constant__ CUtensorMap tmap_q,
             const uint32_t p_tmem = tmem + t * 128;
             // the tile's first P.V overwrites O: the epilogue must have drained the previous one
             if (jn == 0 && tdone > 0) SV_MMA_WAIT(o_free + t, (tdone - 1) & 1);
+#if SV_LEAN
+            // O_t += P_t V_j: every softmax thread arrives on the first-half barrier before the
+            // second, so waiting on the second covers all of P (one wait + fence per op: the
+            // issue queue is shallow, every instruction here is tensor-pipe idle time)
+            SV_MMA_WAIT(p_bar + 2 * t + 1, par);
+            tc_fence_after();
+            if (leader) {
+#pragma unroll
+              for (int kk = 0; kk < BLK / 16; ++kk)
+                mma_ts(o_tmem, p_tmem + kk * 8, dv + ((uint32_t)(kk * 2048) >> 4), IDESC_PV,
+                       (jn > 0 || kk > 0) ? 1u : 0u);
+              mma_commit(kv_empty + sv);
+            }
+#else
             // O_t += P_t V_j in two halves: the first as soon as half of P is in TMEM
             SV_MMA_WAIT(p_bar + 2 * t, par);
             tc_fence_after();
@@ -652,6 +690,7 @@ attn_fwd_kernel(const __grid_constant__ CUtensorMap tmap_q,
               mma_commit(kv_empty + sv);
             }
             __syncwarp();
+#endif
             if (more) {
               if (t) ++jn1; else ++jn0;
               issue_qk(t, sk, qb, jn + 2 == nn);
@@ -664,7 +703,6 @@ attn_fwd_kernel(const __grid_constant__ CUtensorMap tmap_q,
           }
         }
       }
-      reg_alloc<REG_LAUNCH>();
     } else {
       // ---------------------------------------------------------------- softmax warpgroups
       reg_alloc<REG_SOFTMAX>();
@@ -835,6 +873,10 @@ attn_fwd_kernel(const __grid_constant__ CUtensorMap tmap_q,
       reg_dealloc<REG_LAUNCH>();
     }
     __syncthreads();
+    // WG2/WG3 take their registers back only once every softmax warp has returned its share:
+    // a producer that finished early and re-grew inside its branch could starve a softmax warp
+    // that had not grown yet (setmaxnreg.inc blocks until the CTA pool has the registers).
+    if (warp >= WARP_MMA) reg_alloc<REG_LAUNCH>();
   }
 
   tc_fence_before();

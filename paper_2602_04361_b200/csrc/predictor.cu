@@ -230,7 +230,8 @@ predict_kernel(const __grid_constant__ CUtensorMap tmap_q,
         }
       }
     }
-    reg_alloc<REG_LAUNCH>();
+    // no re-grow here: a loader that finished early would race the softmax warps' growth for
+    // the CTA's register pool (setmaxnreg.inc blocks), and nothing after this needs registers
   } else {
     // ---------------------------------------------------------------- softmax warpgroups
     reg_alloc<REG_SOFTMAX>();

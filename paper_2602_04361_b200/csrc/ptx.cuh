@@ -54,8 +54,8 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   const uint64_t t0 = globaltimer_ns();
   while (!mbar_try_wait(a, parity)) {
     if (globaltimer_ns() - t0 > 4000000000ull) {
-      printf("sparvar: mbarrier wait timeout (block %d,%d thread %d parity %u)\n", blockIdx.x,
-             blockIdx.y, threadIdx.x, parity);
+      printf("sparvar: mbarrier wait timeout (block %d,%d thread %d parity %u smem 0x%x)\n",
+             blockIdx.x, blockIdx.y, threadIdx.x, parity, a);
       __trap();
     }
   }
