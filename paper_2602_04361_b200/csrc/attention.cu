@@ -41,7 +41,7 @@ extern "C" int sparvar_prof_read(long long* host, int n) {
   return cudaMemcpyFromSymbol(host, sv_prof_buf, sizeof(long long) * n) == cudaSuccess ? 0 : 1;
 }
 #define SV_STAMP(i_) \
-  if (blockIdx.x == 0 && threadIdx.x == 0 && (i_) < 7000) sv_prof_buf[(i_)] = clock64();
+  if (blockIdx.x == 0 && threadIdx.x == 0 && (i_) < 5000) sv_prof_buf[(i_)] = clock64();
 #define SV_STAMP_CTA(base_) \
   if (threadIdx.x == 0 && blockIdx.x < 192) sv_prof_buf[(base_) + blockIdx.x] = (long long)globaltimer_ns();
 #define SV_ACC(base_, v_) \
@@ -111,6 +111,13 @@ constexpr int ORDER = SV_ORDER;
 #else
 #define SV_MMA_WAIT mbar_wait
 #endif
+// profiling builds: clocks the MMA issuer spends blocked, per barrier kind (base index)
+#define SV_MMA_WAIT_T(bar_, par_, base_)                                   \
+  {                                                                        \
+    const long long t0_ = SV_CLK();                                        \
+    SV_MMA_WAIT(bar_, par_);                                               \
+    if ((threadIdx.x & 31) == 0) SV_ACC(base_, SV_CLK() - t0_)             \
+  }
 
 __host__ __device__ inline int gcd_int(int a, int b) {
   while (b) { const int t = a % b; a = b; b = t; }
@@ -465,7 +472,9 @@ attn_fwd_kernel(const __grid_constant__ CUtensorMap tmap_q,
         mbar_wait(st_bar + t, par);
         const float2 stt = sm->stats[t][row];
         mbar_arrive(st_free + t);
+        const long long te0_ = SV_CLK();
         mbar_wait(o_bar + t, par);
+        if ((threadIdx.x & 127) == 0) SV_ACC(5400, SV_CLK() - te0_)
         tc_fence_after();
         const int n_row = tile * BM + row;
         const bool store = n_row < a.n_q;
@@ -507,7 +516,11 @@ attn_fwd_kernel(const __grid_constant__ CUtensorMap tmap_q,
             const int s = kv_idx % C::NST;
             const uint32_t ph = (kv_idx / C::NST) & 1;
             ++kv_idx;
-            mbar_wait(kv_empty + s, ph ^ 1);
+            {
+              const long long t0_ = SV_CLK();
+              mbar_wait(kv_empty + s, ph ^ 1);
+              SV_ACC(5000, SV_CLK() - t0_)
+            }
             uint8_t* dst = sKV + s * C::STAGE_BYTES;
             mbar_arrive_expect_tx(kv_full + s, C::STAGE_BYTES);
 #pragma unroll
@@ -599,7 +612,7 @@ attn_fwd_kernel(const __grid_constant__ CUtensorMap tmap_q,
         uint32_t ring_ph = (kv_idx / C::NST) & 1;
         auto next_stage = [&]() -> uint32_t {
           const int s = ring_s;
-          SV_MMA_WAIT(kv_full + s, ring_ph);
+          SV_MMA_WAIT_T(kv_full + s, ring_ph, 6000);
           if (++ring_s == C::NST) { ring_s = 0; ring_ph ^= 1; }
           ++kv_idx;
           return (uint32_t)s;
@@ -633,10 +646,11 @@ attn_fwd_kernel(const __grid_constant__ CUtensorMap tmap_q,
           const int n = sm->n[ic];
           if (t) { qb1 = qb; nn1 = n; jn1 = 0; } else { qb0 = qb; nn0 = n; jn0 = 0; }
           const uint32_t s = next_stage();
-          SV_MMA_WAIT(q_full + qb, (meta >> 3) & 1);
+          SV_MMA_WAIT_T(q_full + qb, (meta >> 3) & 1, 6600);
           tc_fence_after();
           issue_qk(t, s, qb, n == 1);
         };
+        const long long tm0_ = SV_CLK();
         start(0, 0);
         start(1, 0);
         while (icur0 >= 0 || icur1 >= 0) {
@@ -652,16 +666,17 @@ attn_fwd_kernel(const __grid_constant__ CUtensorMap tmap_q,
             const uint32_t sk = more ? next_stage() : 0u;
             const uint32_t par = (t ? p_cnt1 : p_cnt0) & 1;
             if (t) ++p_cnt1; else ++p_cnt0;
+            if (lane == 0) SV_ACC(7000, 1)
             const uint64_t dv = dv0 + ((uint64_t)(sv * C::STAGE_BYTES) >> 4);
             const uint32_t o_tmem = tmem + 256 + t * D;
             const uint32_t p_tmem = tmem + t * 128;
             // the tile's first P.V overwrites O: the epilogue must have drained the previous one
-            if (jn == 0 && tdone > 0) SV_MMA_WAIT(o_free + t, (tdone - 1) & 1);
+            if (jn == 0 && tdone > 0) SV_MMA_WAIT_T(o_free + t, (tdone - 1) & 1, 6400);
 #if SV_LEAN
             // O_t += P_t V_j: every softmax thread arrives on the first-half barrier before the
             // second, so waiting on the second covers all of P (one wait + fence per op: the
             // issue queue is shallow, every instruction here is tensor-pipe idle time)
-            SV_MMA_WAIT(p_bar + 2 * t + 1, par);
+            SV_MMA_WAIT_T(p_bar + 2 * t + 1, par, 6200);
             tc_fence_after();
             if (leader) {
 #pragma unroll
@@ -702,6 +717,7 @@ attn_fwd_kernel(const __grid_constant__ CUtensorMap tmap_q,
             }
           }
         }
+        if (lane == 0) SV_ACC(6800, SV_CLK() - tm0_)
       }
     } else {
       // ---------------------------------------------------------------- softmax warpgroups
@@ -729,7 +745,9 @@ attn_fwd_kernel(const __grid_constant__ CUtensorMap tmap_q,
         int j = 0;
         while (have) {
           SV_STAMP(5 * s_cnt + 0)
+          const long long ts0_ = SV_CLK();
           mbar_wait(s_bar + t, s_cnt & 1);
+          if ((threadIdx.x & 127) == 0) SV_ACC(5200, SV_CLK() - ts0_)
           SV_STAMP(5 * s_cnt + 1)
           ++s_cnt;
           tc_fence_after();
