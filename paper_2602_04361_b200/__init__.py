@@ -51,7 +51,9 @@ class _Shape(ctypes.Structure):
                 ("o_stride_bh", ctypes.c_int64)]
 
 
-def _load(path: str = LIB_PATH):
+def _load(path: str = LIB_PATH, partial: bool = False):
+    """Bind the C ABI of libsparvar.so.  `partial` (development timing of older variant builds
+    only) skips entry points the library does not export."""
     if not os.path.exists(path):
         raise ImportError(f"{path} not built: run `python -m paper_2602_04361_b200.build`")
     L = ctypes.CDLL(path)
@@ -70,6 +72,8 @@ def _load(path: str = LIB_PATH):
                                              P, P],
     }
     for name, args in sig.items():
+        if partial and not hasattr(L, name):
+            continue
         f = getattr(L, name)
         f.argtypes = args
         f.restype = ctypes.c_int

@@ -56,6 +56,8 @@ CASES = [
     (TINY, 16, 0, 1, 0.0), (TINY, 16, 1, 0, 0.02),
     (EQ256, 32, 0, 2, 0.0), (EQ256, 32, 1, 0, 0.05), (EQ256, 16, 0, 3, 0.0),
     (INF2B, 128, 0, 5, 0.0), (INF2B, 128, 1, 0, 0.015), (INF2B, 64, 0, 7, 0.0),
+    # a single ragged query tile (64 rows) and a ragged last KV block at B in {64, 128}
+    (EQ256, 64, 0, 2, 0.0), (EQ256, 128, 1, 0, 0.05),
 ]
 
 
