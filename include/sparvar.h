@@ -176,6 +176,22 @@ sparvar_status sparvar_cache_residual(const sparvar_schedule* sched, int32_t dec
                                      const int32_t* col_idx_S, float softmax_scale,
                                      uint16_t* o_scratch, uint16_t* o_cache, void* stream);
 
+/* NEXT(1)/NEXT(3) — the same O_cache when the dense attention at S has already been computed
+ *   (the decision scale runs dense attention in every layer): o_dense is that
+ *   output (bf16 [BH][N_S][D], o_stride_bh), read only; o_cache receives
+ *   o_dense - Softmax(Q K_inds^T) V_inds (the block-sparse term is computed into o_cache and
+ *   subtracted in place, fp32, bf16 result).  o_cache must not alias o_dense.  Errors as for
+ *   sparvar_cache_residual.
+ */
+sparvar_status sparvar_cache_residual_from_dense(const sparvar_schedule* sched,
+                                                int32_t decision_scale, int32_t block,
+                                                const sparvar_attn_shape* shape,
+                                                const uint16_t* q_S, const uint16_t* k_cache,
+                                                const uint16_t* v_cache, const int32_t* row_ptr_S,
+                                                const int32_t* col_idx_S, float softmax_scale,
+                                                const uint16_t* o_dense, uint16_t* o_cache,
+                                                void* stream);
+
 /* NEXT(1) — cached block-sparse attention at scale K:
  *   O^(K) = Upsample(O_cache) + Delta O^(K), Delta O^(K) = sparvar_block_sparse_attn output.
  *   Upsample is nearest neighbour over the query grid: output query (x, y) of side s_K adds

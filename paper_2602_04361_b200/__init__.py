@@ -22,7 +22,7 @@ import torch
 __all__ = [
     "lib", "SparVARError", "geometry", "local_mask", "predict_pattern", "map_indices",
     "build_block_lists", "block_sparse_attn", "dense_attn", "cache_residual",
-    "block_sparse_attn_cached", "SparseLayer", "unpack_bits",
+    "block_sparse_attn_cached", "cache_residual_from_dense", "SparseLayer", "unpack_bits",
     "SELECT_TOPK", "SELECT_THRESHOLD", "MAP_FOOTPRINT", "MAP_POINT",
 ]
 
@@ -70,6 +70,7 @@ def _load(path: str = LIB_PATH, partial: bool = False):
         "sparvar_cache_residual": [S, I32, I32, SH, P, P, P, P, P, F32, P, P, P],
         "sparvar_block_sparse_attn_cached": [S, I32, I32, SH, P, P, P, P, P, F32, P, I32, I64, P,
                                              P, P],
+        "sparvar_cache_residual_from_dense": [S, I32, I32, SH, P, P, P, P, P, F32, P, P, P],
     }
     for name, args in sig.items():
         if partial and not hasattr(L, name):
@@ -243,6 +244,25 @@ def cache_residual(sides, decision_scale: int, block: int, q_S, k_cache, v_cache
                                       ctypes.byref(sh), _ptr(q_S), _ptr(k_cache), _ptr(v_cache),
                                       _ptr(row_ptr_S), _ptr(col_idx_S), softmax_scale,
                                       _ptr(o_scratch), _ptr(o_cache), _stream(stream)))
+    return o_cache
+
+
+def cache_residual_from_dense(sides, decision_scale: int, block: int, q_S, k_cache, v_cache,
+                              row_ptr_S, col_idx_S, o_dense, softmax_scale: float = 0.0,
+                              o_cache=None, stream=None):
+    """NEXT(1)/NEXT(3): O_cache = o_dense - O_sparse at S, reusing the decision scale's dense
+    output instead of recomputing it."""
+    if o_cache is None:
+        o_cache = torch.empty_like(q_S)
+    if _bh_view(v_cache, "v_cache") != k_cache.stride(0):
+        raise ValueError("k_cache and v_cache must share a (b,h) stride")
+    if _bh_view(o_dense, "o_dense") != o_cache.stride(0):
+        raise ValueError("o_dense and o_cache must share a (b,h) stride")
+    sh = _attn_shape(q_S, k_cache, o_cache)
+    _check(lib.sparvar_cache_residual_from_dense(
+        ctypes.byref(_sched(sides)), decision_scale, block, ctypes.byref(sh), _ptr(q_S),
+        _ptr(k_cache), _ptr(v_cache), _ptr(row_ptr_S), _ptr(col_idx_S), softmax_scale,
+        _ptr(o_dense), _ptr(o_cache), _stream(stream)))
     return o_cache
 
 

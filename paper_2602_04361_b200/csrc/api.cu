@@ -122,7 +122,7 @@ extern "C" {
 
 const char* sparvar_last_error(void) { return g_err.c_str(); }
 
-int32_t sparvar_version(void) { return 100; }
+int32_t sparvar_version(void) { return 101; }   // 1.01: + sparvar_cache_residual_from_dense
 
 sparvar_status sparvar_local_mask(const sparvar_schedule* sched, int32_t target_scale,
                                   int32_t block, int32_t sink_scales, const int32_t* windows,
@@ -337,6 +337,30 @@ sparvar_status sparvar_cache_residual(const sparvar_schedule* sched, int32_t dec
   const int side = sched->sides[decision_scale - 1];
   cudaError_t e = sv::launch_residual(shape->batch_heads, side * side, shape->head_dim, o_cache,
                                       shape->o_stride_bh, o_scratch, shape->o_stride_bh, o_cache,
+                                      shape->o_stride_bh, (cudaStream_t)stream);
+  if (e != cudaSuccess) return cuda_fail(e, "residual launch");
+  return ok();
+}
+
+sparvar_status sparvar_cache_residual_from_dense(const sparvar_schedule* sched,
+                                                int32_t decision_scale, int32_t block,
+                                                const sparvar_attn_shape* shape,
+                                                const uint16_t* q_S, const uint16_t* k_cache,
+                                                const uint16_t* v_cache, const int32_t* row_ptr_S,
+                                                const int32_t* col_idx_S, float softmax_scale,
+                                                const uint16_t* o_dense, uint16_t* o_cache,
+                                                void* stream) {
+  if (row_ptr_S == nullptr || col_idx_S == nullptr || o_dense == nullptr || o_cache == nullptr)
+    return fail(SPARVAR_ERR_INVALID_ARG, "null row_ptr / col_idx / o_dense / o_cache");
+  if (o_dense == o_cache) return fail(SPARVAR_ERR_INVALID_ARG, "o_cache must not alias o_dense");
+  if (!aligned16(o_dense)) return fail(SPARVAR_ERR_INVALID_ARG, "o_dense must be 16-byte aligned");
+  // the sparse term lands in o_cache, then o_cache = o_dense - o_cache element by element
+  sparvar_status s = attn_common(sched, decision_scale, block, shape, q_S, k_cache, v_cache,
+                                 row_ptr_S, col_idx_S, softmax_scale, o_cache, nullptr, stream);
+  if (s != SPARVAR_OK) return s;
+  const int side = sched->sides[decision_scale - 1];
+  cudaError_t e = sv::launch_residual(shape->batch_heads, side * side, shape->head_dim, o_dense,
+                                      shape->o_stride_bh, o_cache, shape->o_stride_bh, o_cache,
                                       shape->o_stride_bh, (cudaStream_t)stream);
   if (e != cudaSuccess) return cuda_fail(e, "residual launch");
   return ok();

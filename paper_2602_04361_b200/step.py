@@ -1,0 +1,140 @@
+"""NEXT(3): the attention of the sparsified tail of one generation step
+across all layers, as the paper deploys SparVAR.
+
+Per layer, at the decision scale S the model runs full attention; the target
+scales S+1..K run block-sparse attention:
+
+  CS4A layers (the first round(0.6 L), "substituted from the shallowest"):
+      O_S     = dense attention at S                             (sparvar_dense_attn)
+      pattern = predictor at S (block masses, top-k / threshold) (sparvar_predict_pattern)
+      O_cache = O_S - Softmax(Q_S K_inds^T) V_inds              (sparvar_cache_residual_from_dense)
+      for k in S+1..K:
+          lists_k = CSR(map S->k of the pattern)                 (sparvar_map_indices, _build_block_lists)
+          O_k     = NN-upsample(O_cache) + Delta O_k             (sparvar_block_sparse_attn_cached)
+  CSLA layers (the rest):
+      O_S     = dense attention at S
+      for k in S+1..K:  O_k = block-sparse attention over the CSLA local mask of k
+                        (sparvar_local_mask / _build_block_lists once per step: the mask is the
+                         same for every layer and head)
+
+Every step of the path is a kernel of libsparvar.so; this module only sequences the calls and
+owns the per-step scratch (masks, lists, O_cache), allocated once and reused layer after layer.
+"""
+from __future__ import annotations
+
+from typing import Dict, List, Sequence
+
+import torch
+
+from . import (MAP_FOOTPRINT, SELECT_TOPK, block_sparse_attn, block_sparse_attn_cached,
+               build_block_lists, cache_residual_from_dense, dense_attn, geometry, local_mask,
+               map_indices, predict_pattern)
+
+
+def layer_split(layers: int, cs4a_fraction: float = 0.6) -> int:
+    """Number of CS4A layers (the shallowest ones), PAPER.md:990 ("6:4"), at least 0."""
+    return max(0, min(layers, int(round(cs4a_fraction * layers))))
+
+
+class SparsifiedStep:
+    """Attention of scales S..K of one generation step for `layers` layers (see module doc).
+
+    Inputs per layer l: q[l][k] (bh, N_k, D) bf16 for k in S..K, and the layer's K/V cache
+    (bh, >= C_K, D) bf16.  Outputs out[l][k] (bh, N_k, D) bf16 (caller-allocated or created).
+    """
+
+    def __init__(self, sides: Sequence[int], decision: int, target: int, block: int, bh: int,
+                 layers: int, head_dim: int = 128, cs4a_fraction: float = 0.6,
+                 sink_scales: int = 5, windows=(7, 5, 3, 1, 1), select_mode=SELECT_TOPK,
+                 topk: int = 5, threshold: float = 0.01, map_mode=MAP_FOOTPRINT):
+        if not 1 <= decision < target <= len(sides):
+            raise ValueError("need 1 <= decision < target <= number of scales")
+        self.sides, self.S, self.K, self.B, self.bh = list(sides), decision, target, block, bh
+        self.layers, self.D = layers, head_dim
+        self.n_cs4a = layer_split(layers, cs4a_fraction)
+        self.sink, self.windows = sink_scales, tuple(windows)
+        self.select_mode, self.topk, self.threshold, self.map_mode = select_mode, topk, threshold, map_mode
+        self.targets = list(range(decision + 1, target + 1))
+        dev = "cuda"
+        gS = geometry(sides, decision, block)
+        self.gS = gS
+        self.src = torch.empty((bh, gS["G_q"], gS["W"]), dtype=torch.int32, device=dev)
+        self.lists_S = self._lists(gS)
+        self.o_cache = torch.empty((bh, gS["N"], head_dim), dtype=torch.bfloat16, device=dev)
+        self.g = {k: geometry(sides, k, block) for k in self.targets}
+        self.mapped = {k: torch.empty((bh, g["G_q"], g["W"]), dtype=torch.int32, device=dev)
+                       for k, g in self.g.items()}
+        self.local = {k: torch.empty((g["G_q"], g["W"]), dtype=torch.int32, device=dev)
+                      for k, g in self.g.items()}
+        self.lists_map = {k: self._lists(g) for k, g in self.g.items()}
+        self.lists_csla = {k: self._lists(g) for k, g in self.g.items()}
+        self.status = torch.zeros(1, dtype=torch.int32, device=dev)
+
+    def _lists(self, g):
+        cap = self.bh * g["G_q"] * g["G_kv"]
+        return (torch.empty(self.bh * g["G_q"] + 1, dtype=torch.int32, device="cuda"),
+                torch.empty(cap, dtype=torch.int32, device="cuda"), cap)
+
+    def kind(self, layer: int) -> str:
+        return "cs4a" if layer < self.n_cs4a else "csla"
+
+    def alloc_outputs(self) -> List[Dict[int, torch.Tensor]]:
+        return [{k: torch.empty((self.bh, self.sides[k - 1] ** 2, self.D), dtype=torch.bfloat16,
+                                device="cuda") for k in [self.S] + self.targets}
+                for _ in range(self.layers)]
+
+    def csla_patterns(self, stream=None):
+        """Local masks and their CSR lists for every target scale (once per step)."""
+        for k in self.targets:
+            g = self.g[k]
+            local_mask(self.sides, k, self.B, self.sink, self.windows, out=self.local[k],
+                       stream=stream)
+            rp, ci, cap = self.lists_csla[k]
+            build_block_lists(self.bh, g["G_q"], g["G_kv"], [(self.local[k], True)], cap, rp, ci,
+                              self.status, stream=stream)
+
+    def layer(self, l: int, q: Dict[int, torch.Tensor], k_cache, v_cache,
+              out: Dict[int, torch.Tensor], stream=None):
+        S, B = self.S, self.B
+        dense_attn(self.sides, S, q[S], k_cache, v_cache, o=out[S], stream=stream)
+        if self.kind(l) == "cs4a":
+            gS = self.gS
+            predict_pattern(self.sides, S, B, self.sink, q[S], k_cache, self.select_mode,
+                            self.topk, self.threshold, want_mass=False, mask_out=self.src,
+                            stream=stream)
+            rpS, ciS, capS = self.lists_S
+            build_block_lists(self.bh, gS["G_q"], gS["G_kv"], [(self.src, False)], capS, rpS, ciS,
+                              self.status, stream=stream)
+            cache_residual_from_dense(self.sides, S, B, q[S], k_cache, v_cache, rpS, ciS, out[S],
+                                      o_cache=self.o_cache, stream=stream)
+            for k in self.targets:
+                g = self.g[k]
+                map_indices(self.sides, S, k, B, self.sink, self.src, self.map_mode,
+                            out=self.mapped[k], stream=stream)
+                rp, ci, cap = self.lists_map[k]
+                build_block_lists(self.bh, g["G_q"], g["G_kv"], [(self.mapped[k], False)], cap, rp,
+                                  ci, self.status, stream=stream)
+                block_sparse_attn_cached(self.sides, k, B, q[k], k_cache, v_cache, rp, ci,
+                                         self.o_cache, S, o=out[k], stream=stream)
+        else:
+            for k in self.targets:
+                rp, ci, _ = self.lists_csla[k]
+                block_sparse_attn(self.sides, k, B, q[k], k_cache, v_cache, rp, ci, o=out[k],
+                                  stream=stream)
+
+    def run(self, qs: Sequence[Dict[int, torch.Tensor]], ks: Sequence[torch.Tensor],
+            vs: Sequence[torch.Tensor], outs=None, stream=None):
+        """The whole sparsified tail for all layers; returns outs[l][k]."""
+        if outs is None:
+            outs = self.alloc_outputs()
+        self.csla_patterns(stream)
+        for l in range(self.layers):
+            self.layer(l, qs[l], ks[l], vs[l], outs[l], stream)
+        return outs
+
+    def run_dense(self, qs, ks, vs, outs, stream=None):
+        """The same scales with dense attention everywhere: the step's denominator."""
+        for l in range(self.layers):
+            for k in [self.S] + self.targets:
+                dense_attn(self.sides, k, qs[l][k], ks[l], vs[l], o=outs[l][k], stream=stream)
+        return outs
