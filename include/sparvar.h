@@ -32,6 +32,7 @@
 #define SPARVAR_H_
 
 #include <stdint.h>
+#include <stddef.h>
 
 #ifdef __cplusplus
 extern "C" {
@@ -191,6 +192,28 @@ sparvar_status sparvar_cache_residual_from_dense(const sparvar_schedule* sched,
                                                 const int32_t* col_idx_S, float softmax_scale,
                                                 const uint16_t* o_dense, uint16_t* o_cache,
                                                 void* stream);
+
+/* NEXT(3) — the decision-scale dense pass with the predictor fused in (the
+ *   model runs full attention at S, and the block masses are read off that same softmax):
+ *   o = dense attention at decision_scale (as sparvar_dense_attn, but the key-block size is
+ *   `block`), lse (nullable, fp32 [BH][N_S]) its log-sum-exp, and mass_out (nullable,
+ *   fp32 [BH][G_S][G_kvS]) / mask_out (bit rows [BH][G_S][W_S]) exactly as
+ *   sparvar_predict_pattern defines them (same selection rules and tie breaks; masses from the
+ *   fp32 probabilities before the bf16 rounding of P).  workspace: caller-owned device memory
+ *   of at least sparvar_dense_attn_mass_workspace() bytes, 16-byte aligned (per-row block sums
+ *   and their reference maxima, and the LSE if lse is null).  Errors as for
+ *   sparvar_predict_pattern; SPARVAR_ERR_CAPACITY if the workspace is too small.
+ */
+size_t sparvar_dense_attn_mass_workspace(const sparvar_schedule* sched, int32_t decision_scale,
+                                         int32_t block, int32_t batch_heads);
+sparvar_status sparvar_dense_attn_mass(const sparvar_schedule* sched, int32_t decision_scale,
+                                       int32_t block, int32_t sink_scales,
+                                       const sparvar_attn_shape* shape, const uint16_t* q_S,
+                                       const uint16_t* k_cache, const uint16_t* v_cache,
+                                       float softmax_scale, int32_t select_mode, int32_t topk,
+                                       float threshold, uint16_t* o, float* lse, float* mass_out,
+                                       uint32_t* mask_out, void* workspace, size_t workspace_bytes,
+                                       void* stream);
 
 /* NEXT(1) — cached block-sparse attention at scale K:
  *   O^(K) = Upsample(O_cache) + Delta O^(K), Delta O^(K) = sparvar_block_sparse_attn output.

@@ -22,7 +22,8 @@ import torch
 __all__ = [
     "lib", "SparVARError", "geometry", "local_mask", "predict_pattern", "map_indices",
     "build_block_lists", "block_sparse_attn", "dense_attn", "cache_residual",
-    "block_sparse_attn_cached", "cache_residual_from_dense", "SparseLayer", "unpack_bits",
+    "block_sparse_attn_cached", "cache_residual_from_dense", "dense_attn_mass",
+    "dense_attn_mass_workspace", "SparseLayer", "unpack_bits",
     "SELECT_TOPK", "SELECT_THRESHOLD", "MAP_FOOTPRINT", "MAP_POINT",
 ]
 
@@ -71,6 +72,8 @@ def _load(path: str = LIB_PATH, partial: bool = False):
         "sparvar_block_sparse_attn_cached": [S, I32, I32, SH, P, P, P, P, P, F32, P, I32, I64, P,
                                              P, P],
         "sparvar_cache_residual_from_dense": [S, I32, I32, SH, P, P, P, P, P, F32, P, P, P],
+        "sparvar_dense_attn_mass": [S, I32, I32, I32, SH, P, P, P, F32, I32, I32, F32, P, P, P, P,
+                                    P, ctypes.c_size_t, P],
     }
     for name, args in sig.items():
         if partial and not hasattr(L, name):
@@ -78,6 +81,9 @@ def _load(path: str = LIB_PATH, partial: bool = False):
         f = getattr(L, name)
         f.argtypes = args
         f.restype = ctypes.c_int
+    if hasattr(L, "sparvar_dense_attn_mass_workspace"):
+        L.sparvar_dense_attn_mass_workspace.argtypes = [S, I32, I32, I32]
+        L.sparvar_dense_attn_mass_workspace.restype = ctypes.c_size_t
     L.sparvar_last_error.restype = ctypes.c_char_p
     L.sparvar_version.restype = ctypes.c_int32
     return L
@@ -264,6 +270,40 @@ def cache_residual_from_dense(sides, decision_scale: int, block: int, q_S, k_cac
         _ptr(k_cache), _ptr(v_cache), _ptr(row_ptr_S), _ptr(col_idx_S), softmax_scale,
         _ptr(o_dense), _ptr(o_cache), _stream(stream)))
     return o_cache
+
+
+def dense_attn_mass(sides, decision_scale: int, block: int, sink_scales: int, q_S, k_cache,
+                    v_cache, mode: int = SELECT_TOPK, topk: int = 1, threshold: float = 0.0,
+                    softmax_scale: float = 0.0, o=None, lse=None, want_mass: bool = True,
+                    mass_out=None, mask_out=None, workspace=None, stream=None):
+    """NEXT(3): dense attention at the decision scale with the predictor fused in.  Returns
+    (o, mask, mass or None); mask / mass as predict_pattern's (PAPER.md:264-288)."""
+    g = geometry(sides, decision_scale, block)
+    bh = q_S.shape[0]
+    if o is None:
+        o = torch.empty_like(q_S)
+    if _bh_view(v_cache, "v_cache") != k_cache.stride(0):
+        raise ValueError("k_cache and v_cache must share a (b,h) stride")
+    if mask_out is None:
+        mask_out = torch.empty((bh, g["G_q"], g["W"]), dtype=torch.int32, device="cuda")
+    if want_mass and mass_out is None:
+        mass_out = torch.empty((bh, g["G_q"], g["G_kv"]), dtype=torch.float32, device="cuda")
+    need = dense_attn_mass_workspace(sides, decision_scale, block, bh)
+    if workspace is None:
+        workspace = torch.empty(max(1, need), dtype=torch.uint8, device="cuda")
+    sh = _attn_shape(q_S, k_cache, o)
+    _check(lib.sparvar_dense_attn_mass(
+        ctypes.byref(_sched(sides)), decision_scale, block, sink_scales, ctypes.byref(sh),
+        _ptr(q_S), _ptr(k_cache), _ptr(v_cache), softmax_scale, mode, topk, threshold, _ptr(o),
+        _ptr(lse), _ptr(mass_out if want_mass else None), _ptr(mask_out), _ptr(workspace),
+        workspace.numel() * workspace.element_size(), _stream(stream)))
+    return o, mask_out, (mass_out if want_mass else None)
+
+
+def dense_attn_mass_workspace(sides, decision_scale: int, block: int, bh: int) -> int:
+    """Bytes of device workspace dense_attn_mass needs."""
+    return int(lib.sparvar_dense_attn_mass_workspace(ctypes.byref(_sched(sides)), decision_scale,
+                                                      block, bh))
 
 
 def block_sparse_attn_cached(sides, target: int, block: int, q, k_cache, v_cache, row_ptr,

@@ -122,7 +122,7 @@ extern "C" {
 
 const char* sparvar_last_error(void) { return g_err.c_str(); }
 
-int32_t sparvar_version(void) { return 101; }   // 1.01: + sparvar_cache_residual_from_dense
+int32_t sparvar_version(void) { return 102; }   // 1.02: + sparvar_dense_attn_mass
 
 sparvar_status sparvar_local_mask(const sparvar_schedule* sched, int32_t target_scale,
                                   int32_t block, int32_t sink_scales, const int32_t* windows,
@@ -265,7 +265,8 @@ static sparvar_status attn_common(const sparvar_schedule* sched, int32_t target_
                                   const int32_t* row_ptr, const int32_t* col_idx, float scale_in,
                                   uint16_t* o, float* lse, void* stream,
                                   const uint16_t* add = nullptr, int32_t add_scale = 0,
-                                  int64_t add_stride = 0) {
+                                  int64_t add_stride = 0, float* mass_s = nullptr,
+                                  float* mass_m = nullptr) {
   sv::Geo g;
   sparvar_status s = make_geo(sched, &g);
   if (s != SPARVAR_OK) return s;
@@ -298,6 +299,8 @@ static sparvar_status attn_common(const sparvar_schedule* sched, int32_t target_
   a.add_stride = add_stride;
   a.s_dst = g.side[target_scale - 1];
   a.s_src = add != nullptr ? g.side[add_scale - 1] : 1;
+  a.mass_s = mass_s;
+  a.mass_m = mass_m;
   CUtensorMap tq, tk, tv;
   if ((s = make_tmap(&tq, q, D, n_q, a.bh, shape->q_stride_bh, 128)) != SPARVAR_OK) return s;
   if ((s = make_tmap(&tk, k, D, n_kv, a.bh, shape->kv_stride_bh, block)) != SPARVAR_OK) return s;
@@ -363,6 +366,67 @@ sparvar_status sparvar_cache_residual_from_dense(const sparvar_schedule* sched,
                                       shape->o_stride_bh, o_cache, shape->o_stride_bh, o_cache,
                                       shape->o_stride_bh, (cudaStream_t)stream);
   if (e != cudaSuccess) return cuda_fail(e, "residual launch");
+  return ok();
+}
+
+size_t sparvar_dense_attn_mass_workspace(const sparvar_schedule* sched, int32_t decision_scale,
+                                         int32_t block, int32_t batch_heads) {
+  sv::Geo g;
+  if (make_geo(sched, &g) != SPARVAR_OK || decision_scale < 1 || decision_scale > g.K ||
+      block < 1 || batch_heads < 1)
+    return 0;
+  const long long n_q = (long long)g.side[decision_scale - 1] * g.side[decision_scale - 1];
+  const long long g_kv = ceil_div(g.cum[decision_scale], block);
+  return (size_t)(batch_heads * (2 * g_kv * n_q + n_q)) * sizeof(float);
+}
+
+sparvar_status sparvar_dense_attn_mass(const sparvar_schedule* sched, int32_t decision_scale,
+                                       int32_t block, int32_t sink_scales,
+                                       const sparvar_attn_shape* shape, const uint16_t* q_S,
+                                       const uint16_t* k_cache, const uint16_t* v_cache,
+                                       float softmax_scale, int32_t select_mode, int32_t topk,
+                                       float threshold, uint16_t* o, float* lse, float* mass_out,
+                                       uint32_t* mask_out, void* workspace, size_t workspace_bytes,
+                                       void* stream) {
+  sv::Geo g;
+  sparvar_status s = make_geo(sched, &g);
+  if (s != SPARVAR_OK) return s;
+  if (decision_scale < 1 || decision_scale > g.K)
+    return fail(SPARVAR_ERR_INVALID_ARG, "decision_scale %d not in [1, %d]", decision_scale, g.K);
+  if (sink_scales < 0 || sink_scales > decision_scale)
+    return fail(SPARVAR_ERR_INVALID_ARG, "sink_scales %d not in [0, %d]", sink_scales, decision_scale);
+  if (select_mode != SPARVAR_SELECT_TOPK && select_mode != SPARVAR_SELECT_THRESHOLD)
+    return fail(SPARVAR_ERR_INVALID_ARG, "select_mode %d", select_mode);
+  if (select_mode == SPARVAR_SELECT_TOPK && topk < 1)
+    return fail(SPARVAR_ERR_INVALID_ARG, "topk %d < 1", topk);
+  if (select_mode == SPARVAR_SELECT_THRESHOLD && !std::isfinite(threshold))
+    return fail(SPARVAR_ERR_INVALID_ARG, "threshold must be finite");
+  if (shape == nullptr) return fail(SPARVAR_ERR_INVALID_ARG, "null shape");
+  if (mask_out == nullptr || workspace == nullptr)
+    return fail(SPARVAR_ERR_INVALID_ARG, "null mask_out / workspace");
+  const size_t need = sparvar_dense_attn_mass_workspace(sched, decision_scale, block,
+                                                        shape->batch_heads);
+  if (need == 0 || workspace_bytes < need)
+    return fail(SPARVAR_ERR_CAPACITY, "workspace of %zu bytes < %zu", workspace_bytes, need);
+  if (reinterpret_cast<uintptr_t>(workspace) % 16 != 0)
+    return fail(SPARVAR_ERR_INVALID_ARG, "workspace must be 16-byte aligned");
+  const long long n_q = (long long)g.side[decision_scale - 1] * g.side[decision_scale - 1];
+  const int g_kv = ceil_div(g.cum[decision_scale], block);
+  const int g_q = ceil_div(n_q, block);
+  if (5LL * g_kv * sizeof(float) > 48 * 1024)
+    return fail(SPARVAR_ERR_UNSUPPORTED, "%d key blocks: mass row too wide for shared memory", g_kv);
+  float* ms = static_cast<float*>(workspace);
+  float* mm = ms + (long long)shape->batch_heads * g_kv * n_q;
+  float* lse_ws = mm + (long long)shape->batch_heads * g_kv * n_q;
+  float* lse_use = lse != nullptr ? lse : lse_ws;
+  s = attn_common(sched, decision_scale, block, shape, q_S, k_cache, v_cache, nullptr, nullptr,
+                  softmax_scale, o, lse_use, stream, nullptr, 0, 0, ms, mm);
+  if (s != SPARVAR_OK) return s;
+  const int n_sink_blocks = sink_scales > 0 ? ceil_div(g.cum[sink_scales], block) : 0;
+  cudaError_t e = sv::launch_mass_select(shape->batch_heads, (int)n_q, g_q, g_kv, block, ms, mm,
+                                         lse_use, select_mode, topk, threshold, n_sink_blocks,
+                                         mass_out, mask_out, (cudaStream_t)stream);
+  if (e != cudaSuccess) return cuda_fail(e, "mass select launch");
   return ok();
 }
 

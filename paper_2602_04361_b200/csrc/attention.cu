@@ -265,7 +265,10 @@ __device__ __forceinline__ long long cost_prefix(const AttnArgs& a, int item_beg
   return (long long)(__ldg(a.row_ptr + row) - base_row) + (long long)TILE_OVERHEAD * i;
 }
 
-template <int D, int BLK>
+// MASS (NEXT(3), decision-scale dense pass with fused block mass): every softmax thread also
+// stores, per KV step (= key block v), its row's block sum sum_{j in v} 2^(x_j - m) and the m it
+// is relative to (exp2 domain), for mass_select_kernel to normalise with the row's final LSE.
+template <int D, int BLK, bool MASS = false>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
 attn_fwd_kernel(const __grid_constant__ CUtensorMap tmap_q,
                 const __grid_constant__ CUtensorMap tmap_k,
@@ -737,6 +740,8 @@ attn_fwd_kernel(const __grid_constant__ CUtensorMap tmap_q,
         const int it = item_at(b0 + i);
         Steps<G> st;
         st.init(a, it / n_tiles, it % n_tiles, g_kv);
+        const int mass_row = (it % n_tiles) * BM + row;                    // MASS only
+        const long long mass_base = (long long)(it / n_tiles) * g_kv * a.n_q + mass_row;
         float m = -INFINITY;   // running max of s * scale * log2(e)
         float l = 0.f;         // running sum of exp2(s * sl2 - m)
         int v;
@@ -868,6 +873,13 @@ attn_fwd_kernel(const __grid_constant__ CUtensorMap tmap_q,
             float s0, s1;
             f2_unpack(s2, s0, s1);
             l += s0 + s1;
+            if constexpr (MASS) {
+              if (mass_row < a.n_q) {
+                const long long off = mass_base + (long long)v * a.n_q;
+                a.mass_s[off] = s0 + s1;
+                a.mass_m[off] = mref;
+              }
+            }
           }
           tmem_wait_st();
           tc_fence_before();
@@ -916,11 +928,11 @@ int num_sms() {
   return n;
 }
 
-template <int D, int BLK>
+template <int D, int BLK, bool MASS = false>
 cudaError_t launch_t(const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv,
                      const AttnArgs& a, cudaStream_t st) {
   using C = Cfg<D, BLK>;
-  auto kern = attn_fwd_kernel<D, BLK>;
+  auto kern = attn_fwd_kernel<D, BLK, MASS>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
   if (e != cudaSuccess) return e;
   const int n_tiles = (a.n_q + BM - 1) / BM;
@@ -958,7 +970,81 @@ __global__ void __launch_bounds__(256) residual_kernel(int bh, int rows, int D, 
   }
 }
 
+// NEXT(3): block masses from the MASS pass and the predictor's selection (same rules as
+// predict_kernel: top-k by rank with ties to the smaller v, or mass >= tau |u|, then the sinks).
+// One CTA per (b,h, query block u), thread r = row u*B + r:
+//   mass[u, v] = sum_r s[v][q] * 2^(m[v][q] - lse[q] * log2 e)   (= sum_r sum_{j in v} P[q, j])
+// reduced in a fixed order (warp shuffles, then the 4 warp partials in order): deterministic.
+__global__ void __launch_bounds__(128) mass_select_kernel(int n_q, int g_q, int g_kv, int B,
+                                                          const float* __restrict__ s,
+                                                          const float* __restrict__ m,
+                                                          const float* __restrict__ lse, int mode,
+                                                          int topk, float tau, int n_sink_blocks,
+                                                          float* mass_out, uint32_t* mask_out) {
+  extern __shared__ float shm[];
+  float* part = shm;                  // [4][g_kv]
+  float* mass = shm + 4 * g_kv;       // [g_kv]
+  const int bh = blockIdx.x / g_q, u = blockIdx.x % g_q;
+  const int r = threadIdx.x, warp = r >> 5, lane = r & 31;
+  const int q = u * B + r;
+  const bool valid = r < B && q < n_q;
+  const float L = valid ? lse[(long long)bh * n_q + q] * 1.4426950408889634f : 0.f;
+  const long long base = (long long)bh * g_kv * n_q + q;
+  for (int v = 0; v < g_kv; ++v) {
+    float w = 0.f;
+    if (valid) {
+      const long long off = base + (long long)v * n_q;
+      w = s[off] * exp2f(m[off] - L);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) w += __shfl_xor_sync(0xffffffffu, w, o);
+    if (lane == 0) part[warp * g_kv + v] = w;
+  }
+  __syncthreads();
+  for (int v = r; v < g_kv; v += blockDim.x)
+    mass[v] = ((part[v] + part[g_kv + v]) + part[2 * g_kv + v]) + part[3 * g_kv + v];
+  __syncthreads();
+  if (warp != 0) return;
+  const long long row = (long long)bh * g_q + u;
+  const int W = (g_kv + 31) / 32;
+  const int rows_u = min(B, n_q - u * B);
+  const float thr = tau * float(rows_u);
+  for (int w0 = 0; w0 < W; ++w0) {
+    const int v = w0 * 32 + lane;
+    bool sel = false;
+    if (v < g_kv) {
+      const float mv = mass[v];
+      if (mode == 0) {
+        int rank = 0;
+        for (int t = 0; t < g_kv; ++t) {
+          const float mt = mass[t];
+          rank += (mt > mv) || (mt == mv && t < v);
+        }
+        sel = rank < topk;
+      } else {
+        sel = mv >= thr;
+      }
+      sel = sel || (v < n_sink_blocks);
+      if (mass_out != nullptr) mass_out[row * g_kv + v] = mv;
+    }
+    const uint32_t word = __ballot_sync(0xffffffffu, sel);
+    if (lane == 0) mask_out[row * W + w0] = word;
+  }
+}
+
 }  // namespace
+
+cudaError_t launch_mass_select(int bh, int n_q, int g_q, int g_kv, int B, const float* s,
+                               const float* m, const float* lse, int mode, int topk, float tau,
+                               int n_sink_blocks, float* mass_out, uint32_t* mask_out,
+                               cudaStream_t st) {
+  const size_t shmem = size_t(5) * g_kv * sizeof(float);
+  if (shmem > 48 * 1024) return cudaErrorInvalidValue;
+  if ((long long)bh * g_q <= 0) return cudaSuccess;
+  mass_select_kernel<<<bh * g_q, 128, shmem, st>>>(n_q, g_q, g_kv, B, s, m, lse, mode, topk, tau,
+                                                   n_sink_blocks, mass_out, mask_out);
+  return cudaGetLastError();
+}
 
 cudaError_t launch_residual(int bh, int rows, int D, const uint16_t* dense, long long dense_stride,
                             const uint16_t* sparse, long long sparse_stride, uint16_t* out,
@@ -973,8 +1059,10 @@ cudaError_t launch_residual(int bh, int rows, int D, const uint16_t* dense, long
 
 cudaError_t launch_attention(int head_dim, int block, const CUtensorMap& tq, const CUtensorMap& tk,
                              const CUtensorMap& tv, const AttnArgs& a, cudaStream_t st) {
-#define SV_CASE(D_, B_) \
-  if (head_dim == D_ && block == B_) return launch_t<D_, B_>(tq, tk, tv, a, st);
+#define SV_CASE(D_, B_)                                                   \
+  if (head_dim == D_ && block == B_)                                      \
+    return a.mass_s != nullptr ? launch_t<D_, B_, true>(tq, tk, tv, a, st) \
+                               : launch_t<D_, B_>(tq, tk, tv, a, st);
   SV_CASE(128, 128) SV_CASE(128, 64) SV_CASE(128, 32) SV_CASE(128, 16)
   SV_CASE(64, 128) SV_CASE(64, 64) SV_CASE(64, 32) SV_CASE(64, 16)
 #undef SV_CASE

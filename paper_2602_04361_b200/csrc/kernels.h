@@ -46,7 +46,16 @@ struct AttnArgs {
   const uint16_t* add;   // bf16 [bh][s_src*s_src][D] or nullptr
   long long add_stride;  // elements between (b,h) slabs of add
   int s_src, s_dst;      // query grid sides of the cache (S) and of the output (K)
+  // optional NEXT(3) fused block mass (dense pass at the decision scale): per (bh, block v, row q)
+  // at [(bh * g_kv + v) * n_q + q] the row's sum of 2^(x - m) over the block and that m
+  float* mass_s;
+  float* mass_m;
 };
+// NEXT(3): masses from the MASS pass (+ LSE) and top-k / threshold selection into bit rows
+cudaError_t launch_mass_select(int bh, int n_q, int g_q, int g_kv, int B, const float* s,
+                               const float* m, const float* lse, int mode, int topk, float tau,
+                               int n_sink_blocks, float* mass_out, uint32_t* mask_out,
+                               cudaStream_t st);
 // o_cache = o_dense - o_sparse, bf16 in / out, fp32 arithmetic (NEXT(1))
 cudaError_t launch_residual(int bh, int rows, int D, const uint16_t* dense, long long dense_stride,
                             const uint16_t* sparse, long long sparse_stride, uint16_t* out,

@@ -5,8 +5,9 @@ Per layer, at the decision scale S the model runs full attention (PAPER.md:264-2
 scales S+1..K run block-sparse attention:
 
   CS4A layers (the first round(0.6 L), "substituted from the shallowest"):
-      O_S     = dense attention at S                             (sparvar_dense_attn)
-      pattern = predictor at S (block masses, top-k / threshold) (sparvar_predict_pattern)
+      O_S, pattern = dense attention at S with the block masses read off its softmax and
+                     selected (top-k / threshold)                (sparvar_dense_attn_mass;
+                     fused=False: sparvar_dense_attn + sparvar_predict_pattern)
       O_cache = O_S - Softmax(Q_S K_inds^T) V_inds              (sparvar_cache_residual_from_dense)
       for k in S+1..K:
           lists_k = CSR(map S->k of the pattern)                 (sparvar_map_indices, _build_block_lists)
@@ -27,8 +28,8 @@ from typing import Dict, List, Sequence
 import torch
 
 from . import (MAP_FOOTPRINT, SELECT_TOPK, block_sparse_attn, block_sparse_attn_cached,
-               build_block_lists, cache_residual_from_dense, dense_attn, geometry, local_mask,
-               map_indices, predict_pattern)
+               build_block_lists, cache_residual_from_dense, dense_attn, dense_attn_mass,
+               dense_attn_mass_workspace, geometry, local_mask, map_indices, predict_pattern)
 
 
 def layer_split(layers: int, cs4a_fraction: float = 0.6) -> int:
@@ -46,7 +47,8 @@ class SparsifiedStep:
     def __init__(self, sides: Sequence[int], decision: int, target: int, block: int, bh: int,
                  layers: int, head_dim: int = 128, cs4a_fraction: float = 0.6,
                  sink_scales: int = 5, windows=(7, 5, 3, 1, 1), select_mode=SELECT_TOPK,
-                 topk: int = 5, threshold: float = 0.01, map_mode=MAP_FOOTPRINT):
+                 topk: int = 5, threshold: float = 0.01, map_mode=MAP_FOOTPRINT,
+                 fused: bool = True):
         if not 1 <= decision < target <= len(sides):
             raise ValueError("need 1 <= decision < target <= number of scales")
         self.sides, self.S, self.K, self.B, self.bh = list(sides), decision, target, block, bh
@@ -69,6 +71,9 @@ class SparsifiedStep:
         self.lists_map = {k: self._lists(g) for k, g in self.g.items()}
         self.lists_csla = {k: self._lists(g) for k, g in self.g.items()}
         self.status = torch.zeros(1, dtype=torch.int32, device=dev)
+        self.fused = fused
+        self.ws = torch.empty(max(1, dense_attn_mass_workspace(sides, decision, block, bh)) if fused
+                              else 1, dtype=torch.uint8, device=dev)
 
     def _lists(self, g):
         cap = self.bh * g["G_q"] * g["G_kv"]
@@ -96,12 +101,18 @@ class SparsifiedStep:
     def layer(self, l: int, q: Dict[int, torch.Tensor], k_cache, v_cache,
               out: Dict[int, torch.Tensor], stream=None):
         S, B = self.S, self.B
-        dense_attn(self.sides, S, q[S], k_cache, v_cache, o=out[S], stream=stream)
         if self.kind(l) == "cs4a":
             gS = self.gS
-            predict_pattern(self.sides, S, B, self.sink, q[S], k_cache, self.select_mode,
-                            self.topk, self.threshold, want_mass=False, mask_out=self.src,
-                            stream=stream)
+            if self.fused:
+                dense_attn_mass(self.sides, S, B, self.sink, q[S], k_cache, v_cache,
+                                self.select_mode, self.topk, self.threshold, o=out[S],
+                                want_mass=False, mask_out=self.src, workspace=self.ws,
+                                stream=stream)
+            else:
+                dense_attn(self.sides, S, q[S], k_cache, v_cache, o=out[S], stream=stream)
+                predict_pattern(self.sides, S, B, self.sink, q[S], k_cache, self.select_mode,
+                                self.topk, self.threshold, want_mass=False, mask_out=self.src,
+                                stream=stream)
             rpS, ciS, capS = self.lists_S
             build_block_lists(self.bh, gS["G_q"], gS["G_kv"], [(self.src, False)], capS, rpS, ciS,
                               self.status, stream=stream)
@@ -117,6 +128,7 @@ class SparsifiedStep:
                 block_sparse_attn_cached(self.sides, k, B, q[k], k_cache, v_cache, rp, ci,
                                          self.o_cache, S, o=out[k], stream=stream)
         else:
+            dense_attn(self.sides, S, q[S], k_cache, v_cache, o=out[S], stream=stream)
             for k in self.targets:
                 rp, ci, _ = self.lists_csla[k]
                 block_sparse_attn(self.sides, k, B, q[k], k_cache, v_cache, rp, ci, o=out[k],

@@ -1,7 +1,9 @@
 """NEXT(3) benchmark: the sparsified attention tail of one generation step across all layers
 (paper_2602_04361_b200/step.py), Infinity-2B shape: 32 layers x 16 heads, D=128, schedule to
 64x64, decision scale S=11, targets 12 and 13, B=128, CS4A:CSLA = 6:4 with CS4A on
-the shallowest layers, top-5 blocks per query block at S.  Synthetic
+the shallowest layers, top-5 blocks per query block at S, the predictor
+fused into the decision scale's dense pass (sparvar_dense_attn_mass; the unfused variant is
+timed beside it).  Synthetic
 seeded iid bf16 Q/K/V per layer (no weights: attention only; QKV projections, FFN and the rest
 of the transformer are outside the hot path).  Inputs (1.0 GB of Q + 2.8 GB of K/V) exceed L2.
 
@@ -91,6 +93,12 @@ def main():
     except Exception as e:  # reported, not fatal
         graph_ms = f"capture failed: {e}"
 
+    # the unfused variant: dense attention at S plus the stand-alone predictor
+    st_u = step.SparsifiedStep(SIDES, S, K, B, bh, L, head_dim=D, topk=5, fused=False)
+    for _ in range(args.warmup):
+        st_u.run(qs, ks, vs, outs)
+    unfused_ms = timed(lambda: st_u.run(qs, ks, vs, outs), args.steps)
+
     # per layer kind (one layer of each, repeated), for the breakdown
     st.csla_patterns()
     lay = {}
@@ -99,6 +107,7 @@ def main():
     rec = {"metric": "sparsified attention tail of one generation step (scales 11-13, all layers) ms",
            "value": round(sparse_ms, 4), "unit": "ms/step", "higher_is_better": False,
            "dense_ms": round(dense_ms, 4), "speedup_vs_dense": round(dense_ms / sparse_ms, 3),
+           "unfused_predictor_ms": round(unfused_ms, 4),
            "graph_replay_ms": graph_ms if not isinstance(graph_ms, float) else round(graph_ms, 4),
            "layers": L, "cs4a_layers": st.n_cs4a, "csla_layers": L - st.n_cs4a,
            "cs4a_layer_ms": round(lay["cs4a"], 4), "csla_layer_ms": round(lay["csla"], 4),

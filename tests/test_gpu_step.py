@@ -30,14 +30,15 @@ def test_layer_split(step_mod):
     assert step_mod.layer_split(3) == 2 and step_mod.layer_split(1) == 1
 
 
-@pytest.mark.parametrize("layers", [3])
-def test_sparsified_step_parity(step_mod, layers):
+@pytest.mark.parametrize("fused", [True, False], ids=["fused_mass", "predictor"])
+def test_sparsified_step_parity(step_mod, fused):
+    layers = 3
     cfg = EQ256
     sides, S, K, B, D, sink = cfg["sides"], cfg["S"], cfg["K"], cfg["B"], cfg["D"], cfg["sink"]
     bh = 2
     sched = Schedule(sides)
     st = step_mod.SparsifiedStep(sides, S, K, B, bh, layers, head_dim=D, sink_scales=sink,
-                                 windows=cfg["windows"], topk=2)
+                                 windows=cfg["windows"], topk=2, fused=fused)
     assert [st.kind(l) for l in range(layers)] == ["cs4a", "cs4a", "csla"]
     qs = [{k: q_iid(100 + l, k, 0, bh, sched.N(k), D).cuda() for k in range(S, K + 1)}
           for l in range(layers)]
