@@ -215,6 +215,44 @@ sparvar_status sparvar_dense_attn_mass(const sparvar_schedule* sched, int32_t de
                                        uint32_t* mask_out, void* workspace, size_t workspace_bytes,
                                        void* stream);
 
+/* NEXT(2) — token-granular CS4A, the paper's own CS4A granularity.
+ *   Query blocks are query_block = C contiguous rows (C = 192 in the paper, PAPER.md:842;
+ *   C in {64, 128, 192}); G_k = ceil(N_k / C).  Token bit rows: uint32 words, bit j%32 of word
+ *   j/32 = key token j, ceil(C_k / 32) words per row.
+ * sparvar_token_colsum: A[bh][g][j] = sum_{q in block g} P[q][j] over the keys j < C_S
+ *    in fp32, P = softmax(Q_S K^T * scale); lse_S (fp32 [BH][N_S]) is the
+ *   log-sum-exp of those rows, e.g. the lse output of sparvar_dense_attn at S.  colsum_out: fp32
+ *   [BH][G_S][C_S].  K is read through the same shape/stride rules as the attention calls.
+ * sparvar_token_select: per row g, the topk_tokens largest column sums (ties to the smaller j,
+ *   k >= C_S keeps all) plus the sink tokens j < C_{sink_scales} -> mask_out [BH][G_S][W].
+ * sparvar_token_map: target query block g_K reads source block phi(g_K); every
+ *   selected source token is projected by Decompose-Align-Project (footprint or point mode,
+ *   PAPER.md:853-881) and the sink tokens are added -> dst_mask [BH][G_K][ceil(C_K/32)].
+ *   Compact it to per-block token lists with sparvar_build_block_lists(bh, G_K, C_K, ...).
+ * sparvar_token_sparse_attn: rows of query block g attend exactly the listed tokens
+ *   col_idx[row_ptr[bh*G_K+g] .. row_ptr[bh*G_K+g+1]) (ascending token indices < C_K):
+ *   o = softmax(q K_J^T * scale) V_J, fp32 online softmax, bf16 out; empty lists give 0 rows.
+ */
+sparvar_status sparvar_token_colsum(const sparvar_schedule* sched, int32_t decision_scale,
+                                    int32_t query_block, const sparvar_attn_shape* shape,
+                                    const uint16_t* q_S, const uint16_t* k_cache,
+                                    const float* lse_S, float softmax_scale, float* colsum_out,
+                                    void* stream);
+sparvar_status sparvar_token_select(const sparvar_schedule* sched, int32_t decision_scale,
+                                    int32_t query_block, int32_t sink_scales, int32_t batch_heads,
+                                    const float* colsum, int32_t topk_tokens, uint32_t* mask_out,
+                                    void* stream);
+sparvar_status sparvar_token_map(const sparvar_schedule* sched, int32_t src_scale,
+                                 int32_t dst_scale, int32_t query_block, int32_t sink_scales,
+                                 int32_t map_mode, int32_t batch_heads, const uint32_t* src_mask,
+                                 uint32_t* dst_mask, void* stream);
+sparvar_status sparvar_token_sparse_attn(const sparvar_schedule* sched, int32_t target_scale,
+                                         int32_t query_block, const sparvar_attn_shape* shape,
+                                         const uint16_t* q, const uint16_t* k_cache,
+                                         const uint16_t* v_cache, const int32_t* row_ptr,
+                                         const int32_t* col_idx, float softmax_scale, uint16_t* o,
+                                         void* stream);
+
 /* NEXT(1) — cached block-sparse attention at scale K:
  *   O^(K) = Upsample(O_cache) + Delta O^(K), Delta O^(K) = sparvar_block_sparse_attn output.
  *   Upsample is nearest neighbour over the query grid: output query (x, y) of side s_K adds

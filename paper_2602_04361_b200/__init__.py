@@ -23,7 +23,8 @@ __all__ = [
     "lib", "SparVARError", "geometry", "local_mask", "predict_pattern", "map_indices",
     "build_block_lists", "block_sparse_attn", "dense_attn", "cache_residual",
     "block_sparse_attn_cached", "cache_residual_from_dense", "dense_attn_mass",
-    "dense_attn_mass_workspace", "SparseLayer", "unpack_bits",
+    "dense_attn_mass_workspace", "token_colsum", "token_select", "token_map", "token_sparse_attn",
+    "SparseLayer", "unpack_bits",
     "SELECT_TOPK", "SELECT_THRESHOLD", "MAP_FOOTPRINT", "MAP_POINT",
 ]
 
@@ -74,6 +75,10 @@ def _load(path: str = LIB_PATH, partial: bool = False):
         "sparvar_cache_residual_from_dense": [S, I32, I32, SH, P, P, P, P, P, F32, P, P, P],
         "sparvar_dense_attn_mass": [S, I32, I32, I32, SH, P, P, P, F32, I32, I32, F32, P, P, P, P,
                                     P, ctypes.c_size_t, P],
+        "sparvar_token_colsum": [S, I32, I32, SH, P, P, P, F32, P, P],
+        "sparvar_token_select": [S, I32, I32, I32, I32, P, I32, P, P],
+        "sparvar_token_map": [S, I32, I32, I32, I32, I32, I32, P, P, P],
+        "sparvar_token_sparse_attn": [S, I32, I32, SH, P, P, P, P, P, F32, P, P],
     }
     for name, args in sig.items():
         if partial and not hasattr(L, name):
@@ -304,6 +309,56 @@ def dense_attn_mass_workspace(sides, decision_scale: int, block: int, bh: int) -
     """Bytes of device workspace dense_attn_mass needs."""
     return int(lib.sparvar_dense_attn_mass_workspace(ctypes.byref(_sched(sides)), decision_scale,
                                                       block, bh))
+
+
+# ------------------------------------------------------------------ NEXT(2): token-level CS4A
+def token_colsum(sides, decision_scale: int, C: int, q_S, k_cache, lse_S, softmax_scale=0.0,
+                 out=None, stream=None):
+    """A[bh, g, j] = sum over query block g (C rows) of P[q, j] at S."""
+    N, Ck = sides[decision_scale - 1] ** 2, sum(s * s for s in sides[:decision_scale])
+    bh, D = q_S.shape[0], q_S.shape[2]
+    if out is None:
+        out = torch.empty((bh, -(-N // C), Ck), dtype=torch.float32, device="cuda")
+    sh = _Shape(bh, D, _bh_view(q_S, "q_S"), _bh_view(k_cache, "k_cache"), 0)
+    _check(lib.sparvar_token_colsum(ctypes.byref(_sched(sides)), decision_scale, C,
+                                    ctypes.byref(sh), _ptr(q_S), _ptr(k_cache), _ptr(lse_S),
+                                    softmax_scale, _ptr(out), _stream(stream)))
+    return out
+
+
+def token_select(sides, decision_scale: int, C: int, sink_scales: int, colsum, topk_tokens: int,
+                 out=None, stream=None):
+    bh, G, Ck = colsum.shape
+    if out is None:
+        out = torch.empty((bh, G, -(-Ck // 32)), dtype=torch.int32, device="cuda")
+    _check(lib.sparvar_token_select(ctypes.byref(_sched(sides)), decision_scale, C, sink_scales, bh,
+                                    _ptr(colsum), topk_tokens, _ptr(out), _stream(stream)))
+    return out
+
+
+def token_map(sides, src_scale: int, dst_scale: int, C: int, sink_scales: int, src_mask,
+              mode: int = MAP_FOOTPRINT, out=None, stream=None):
+    bh = src_mask.shape[0]
+    G_K = -(-(sides[dst_scale - 1] ** 2) // C)
+    Ck = sum(s * s for s in sides[:dst_scale])
+    if out is None:
+        out = torch.empty((bh, G_K, -(-Ck // 32)), dtype=torch.int32, device="cuda")
+    _check(lib.sparvar_token_map(ctypes.byref(_sched(sides)), src_scale, dst_scale, C, sink_scales,
+                                 mode, bh, _ptr(src_mask), _ptr(out), _stream(stream)))
+    return out
+
+
+def token_sparse_attn(sides, target: int, C: int, q, k_cache, v_cache, row_ptr, col_idx,
+                      softmax_scale: float = 0.0, o=None, stream=None):
+    if o is None:
+        o = torch.empty_like(q)
+    if _bh_view(v_cache, "v_cache") != k_cache.stride(0):
+        raise ValueError("k_cache and v_cache must share a (b,h) stride")
+    sh = _attn_shape(q, k_cache, o)
+    _check(lib.sparvar_token_sparse_attn(ctypes.byref(_sched(sides)), target, C, ctypes.byref(sh),
+                                         _ptr(q), _ptr(k_cache), _ptr(v_cache), _ptr(row_ptr),
+                                         _ptr(col_idx), softmax_scale, _ptr(o), _stream(stream)))
+    return o
 
 
 def block_sparse_attn_cached(sides, target: int, block: int, q, k_cache, v_cache, row_ptr,

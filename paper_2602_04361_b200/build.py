@@ -19,7 +19,7 @@ CSRC = os.path.join(HERE, "csrc")
 ROOT = os.path.dirname(HERE)
 LIB = os.path.join(HERE, "libsparvar.so")
 BUILD = os.path.join(HERE, "build")
-SOURCES = ["api.cu", "attention.cu", "predictor.cu", "masks.cu"]
+SOURCES = ["api.cu", "attention.cu", "predictor.cu", "masks.cu", "token.cu"]
 HEADERS = ["ptx.cuh", "kernels.h", "kernel_util.cuh"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",

@@ -122,7 +122,7 @@ extern "C" {
 
 const char* sparvar_last_error(void) { return g_err.c_str(); }
 
-int32_t sparvar_version(void) { return 102; }   // 1.02: + sparvar_dense_attn_mass
+int32_t sparvar_version(void) { return 103; }   // 1.03: + token-level CS4A (NEXT(2))
 
 sparvar_status sparvar_local_mask(const sparvar_schedule* sched, int32_t target_scale,
                                   int32_t block, int32_t sink_scales, const int32_t* windows,
@@ -366,6 +366,128 @@ sparvar_status sparvar_cache_residual_from_dense(const sparvar_schedule* sched,
                                       shape->o_stride_bh, o_cache, shape->o_stride_bh, o_cache,
                                       shape->o_stride_bh, (cudaStream_t)stream);
   if (e != cudaSuccess) return cuda_fail(e, "residual launch");
+  return ok();
+}
+
+// ---------------------------------------------------------------- NEXT(2): token-level CS4A
+static bool token_c_ok(int C) { return C == 64 || C == 128 || C == 192; }
+
+sparvar_status sparvar_token_colsum(const sparvar_schedule* sched, int32_t decision_scale,
+                                    int32_t query_block, const sparvar_attn_shape* shape,
+                                    const uint16_t* q_S, const uint16_t* k_cache,
+                                    const float* lse_S, float softmax_scale, float* colsum_out,
+                                    void* stream) {
+  sv::Geo g;
+  sparvar_status s = make_geo(sched, &g);
+  if (s != SPARVAR_OK) return s;
+  const int S = decision_scale;
+  if (S < 1 || S > g.K) return fail(SPARVAR_ERR_INVALID_ARG, "decision_scale %d not in [1, %d]", S, g.K);
+  if (!token_c_ok(query_block))
+    return fail(SPARVAR_ERR_UNSUPPORTED, "query_block %d not in {64, 128, 192}", query_block);
+  const long long n_q = (long long)g.side[S - 1] * g.side[S - 1];
+  const long long n_kv = g.cum[S];
+  s = check_shape(shape, n_q, n_kv, false);
+  if (s != SPARVAR_OK) return s;
+  if (q_S == nullptr || k_cache == nullptr || lse_S == nullptr || colsum_out == nullptr)
+    return fail(SPARVAR_ERR_INVALID_ARG, "null pointer");
+  if (!aligned16(q_S) || !aligned16(k_cache))
+    return fail(SPARVAR_ERR_INVALID_ARG, "tensor pointers must be 16-byte aligned");
+  const int D = shape->head_dim;
+  const float scale = softmax_scale > 0.f ? softmax_scale : 1.0f / std::sqrt((float)D);
+  CUtensorMap tk, tq;
+  if ((s = make_tmap(&tk, k_cache, D, n_kv, shape->batch_heads, shape->kv_stride_bh, 128)) != SPARVAR_OK)
+    return s;
+  if ((s = make_tmap(&tq, q_S, D, n_q, shape->batch_heads, shape->q_stride_bh, query_block)) != SPARVAR_OK)
+    return s;
+  cudaError_t e = sv::launch_colsum(D, query_block, tk, tq, shape->batch_heads, (int)n_q, (int)n_kv,
+                                    scale * 1.4426950408889634f, lse_S, colsum_out,
+                                    (cudaStream_t)stream);
+  if (e != cudaSuccess) return cuda_fail(e, "colsum launch");
+  return ok();
+}
+
+sparvar_status sparvar_token_select(const sparvar_schedule* sched, int32_t decision_scale,
+                                    int32_t query_block, int32_t sink_scales, int32_t batch_heads,
+                                    const float* colsum, int32_t topk_tokens, uint32_t* mask_out,
+                                    void* stream) {
+  sv::Geo g;
+  sparvar_status s = make_geo(sched, &g);
+  if (s != SPARVAR_OK) return s;
+  const int S = decision_scale;
+  if (S < 1 || S > g.K) return fail(SPARVAR_ERR_INVALID_ARG, "decision_scale %d not in [1, %d]", S, g.K);
+  if (query_block < 1) return fail(SPARVAR_ERR_INVALID_ARG, "query_block %d < 1", query_block);
+  if (sink_scales < 0 || sink_scales > S)
+    return fail(SPARVAR_ERR_INVALID_ARG, "sink_scales %d not in [0, %d]", sink_scales, S);
+  if (topk_tokens < 1) return fail(SPARVAR_ERR_INVALID_ARG, "topk_tokens %d < 1", topk_tokens);
+  if (batch_heads < 1 || batch_heads > 65535)
+    return fail(SPARVAR_ERR_INVALID_ARG, "batch_heads %d", batch_heads);
+  if (colsum == nullptr || mask_out == nullptr) return fail(SPARVAR_ERR_INVALID_ARG, "null pointer");
+  const long long n_q = (long long)g.side[S - 1] * g.side[S - 1];
+  const int G = ceil_div(n_q, query_block);
+  const int n_sink = sink_scales > 0 ? g.cum[sink_scales] : 0;
+  cudaError_t e = sv::launch_topk_tokens(batch_heads * G, g.cum[S], topk_tokens, n_sink, colsum,
+                                         mask_out, (cudaStream_t)stream);
+  if (e != cudaSuccess) return cuda_fail(e, "token select launch");
+  return ok();
+}
+
+sparvar_status sparvar_token_map(const sparvar_schedule* sched, int32_t src_scale,
+                                 int32_t dst_scale, int32_t query_block, int32_t sink_scales,
+                                 int32_t map_mode, int32_t batch_heads, const uint32_t* src_mask,
+                                 uint32_t* dst_mask, void* stream) {
+  sv::Geo g;
+  sparvar_status s = make_geo(sched, &g);
+  if (s != SPARVAR_OK) return s;
+  if (src_scale < 1 || dst_scale > g.K || src_scale > dst_scale)
+    return fail(SPARVAR_ERR_INVALID_ARG, "need 1 <= src_scale (%d) <= dst_scale (%d) <= %d",
+                src_scale, dst_scale, g.K);
+  if (query_block < 1) return fail(SPARVAR_ERR_INVALID_ARG, "query_block %d < 1", query_block);
+  if (sink_scales < 0 || sink_scales > dst_scale)
+    return fail(SPARVAR_ERR_INVALID_ARG, "sink_scales %d not in [0, %d]", sink_scales, dst_scale);
+  if (map_mode != SPARVAR_MAP_FOOTPRINT && map_mode != SPARVAR_MAP_POINT)
+    return fail(SPARVAR_ERR_INVALID_ARG, "map_mode %d", map_mode);
+  if (batch_heads < 1 || batch_heads > 65535)
+    return fail(SPARVAR_ERR_INVALID_ARG, "batch_heads %d", batch_heads);
+  if (src_mask == nullptr || dst_mask == nullptr) return fail(SPARVAR_ERR_INVALID_ARG, "null mask pointer");
+  cudaError_t e = sv::launch_map_tokens(g, src_scale, dst_scale, query_block, sink_scales, map_mode,
+                                        batch_heads, src_mask, dst_mask, (cudaStream_t)stream);
+  if (e == cudaErrorInvalidValue)
+    return fail(SPARVAR_ERR_UNSUPPORTED, "token row of %d bits too wide for shared memory", g.cum[dst_scale]);
+  if (e != cudaSuccess) return cuda_fail(e, "token map launch");
+  return ok();
+}
+
+sparvar_status sparvar_token_sparse_attn(const sparvar_schedule* sched, int32_t target_scale,
+                                         int32_t query_block, const sparvar_attn_shape* shape,
+                                         const uint16_t* q, const uint16_t* k_cache,
+                                         const uint16_t* v_cache, const int32_t* row_ptr,
+                                         const int32_t* col_idx, float softmax_scale, uint16_t* o,
+                                         void* stream) {
+  sv::Geo g;
+  sparvar_status s = make_geo(sched, &g);
+  if (s != SPARVAR_OK) return s;
+  const int K = target_scale;
+  if (K < 1 || K > g.K) return fail(SPARVAR_ERR_INVALID_ARG, "target_scale %d not in [1, %d]", K, g.K);
+  if (!token_c_ok(query_block))
+    return fail(SPARVAR_ERR_UNSUPPORTED, "query_block %d not in {64, 128, 192}", query_block);
+  const long long n_q = (long long)g.side[K - 1] * g.side[K - 1];
+  s = check_shape(shape, n_q, g.cum[K], true);
+  if (s != SPARVAR_OK) return s;
+  if (q == nullptr || k_cache == nullptr || v_cache == nullptr || o == nullptr ||
+      row_ptr == nullptr || col_idx == nullptr)
+    return fail(SPARVAR_ERR_INVALID_ARG, "null pointer");
+  if (!aligned16(q) || !aligned16(k_cache) || !aligned16(v_cache) || !aligned16(o))
+    return fail(SPARVAR_ERR_INVALID_ARG, "tensor pointers must be 16-byte aligned");
+  const int D = shape->head_dim;
+  const float scale = softmax_scale > 0.f ? softmax_scale : 1.0f / std::sqrt((float)D);
+  CUtensorMap tq;
+  if ((s = make_tmap(&tq, q, D, n_q, shape->batch_heads, shape->q_stride_bh, 128)) != SPARVAR_OK)
+    return s;
+  cudaError_t e = sv::launch_token_attn(D, tq, k_cache, v_cache, shape->kv_stride_bh,
+                                        shape->batch_heads, (int)n_q, query_block,
+                                        scale * 1.4426950408889634f, row_ptr, col_idx, o,
+                                        shape->o_stride_bh, (cudaStream_t)stream);
+  if (e != cudaSuccess) return cuda_fail(e, "token attention launch");
   return ok();
 }
 

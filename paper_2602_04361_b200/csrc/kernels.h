@@ -63,6 +63,21 @@ cudaError_t launch_residual(int bh, int rows, int D, const uint16_t* dense, long
 cudaError_t launch_attention(int head_dim, int block, const CUtensorMap& tq, const CUtensorMap& tk,
                              const CUtensorMap& tv, const AttnArgs& a, cudaStream_t st);
 
+// ------------------------------------------------------------------ NEXT(2): token-level CS4A
+// masks.cu: top-k of column-sum rows -> token bit rows; token-level mapping S -> K
+cudaError_t launch_topk_tokens(int rows, int n, int k_tok, int n_sink, const float* a,
+                               uint32_t* out, cudaStream_t st);
+cudaError_t launch_map_tokens(const Geo& g, int S, int K, int C, int sink_scales, int mode,
+                              int bh, const uint32_t* src, uint32_t* dst, cudaStream_t st);
+// token.cu: column sums at S (needs the LSE of the dense pass) and token-list attention at K
+cudaError_t launch_colsum(int head_dim, int C, const CUtensorMap& tk, const CUtensorMap& tq,
+                          int bh, int n_q, int n_kv, float scale_log2, const float* lse,
+                          float* out, cudaStream_t st);
+cudaError_t launch_token_attn(int head_dim, const CUtensorMap& tq, const uint16_t* k,
+                              const uint16_t* v, long long kv_stride, int bh, int n_q, int C,
+                              float scale_log2, const int* row_ptr, const int* col_idx,
+                              uint16_t* o, long long o_stride, cudaStream_t st);
+
 // ------------------------------------------------------------------ predictor.cu
 struct PredArgs {
   int n_q;            // N_S

@@ -230,6 +230,102 @@ __global__ void map_kernel(const Geo g, int S, int K, int B, int sink_scales, in
   for (int w = threadIdx.x; w < W_K; w += blockDim.x) drow[w] = srow[w];
 }
 
+// ------------------------------------------------------------------------ NEXT(2): token level
+// TopK of one column-sum row A^(S)[g, :] (READING 11): one CTA per
+// (b,h,g).  The k-th largest value is found by a 4 x 8-bit radix select on the float bits
+// (column sums are >= 0, so their bit patterns order like the values); every value above it is
+// kept, and of the values equal to it the ones with the smallest indices (ties to the smaller
+// j), then the sink tokens j < C_sink are added.  Output: bit row of ceil(n/32) words.
+constexpr int TK_THREADS = 256;
+
+__global__ void __launch_bounds__(TK_THREADS) topk_tokens_kernel(const float* __restrict__ a, int n,
+                                                                 int k_tok, int n_sink,
+                                                                 uint32_t* __restrict__ out) {
+  __shared__ unsigned hist[256];
+  __shared__ unsigned s_prefix, s_remaining;
+  __shared__ int s_warp[TK_THREADS / 32];
+  const long long row = blockIdx.x;
+  const float* x = a + row * n;
+  const int W = (n + 31) / 32;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  unsigned prefix = 0, mask = 0, remaining = (unsigned)min(k_tok, n);
+  const bool all = k_tok >= n;
+  if (!all) {
+    for (int shift = 24; shift >= 0; shift -= 8) {
+      for (int b = threadIdx.x; b < 256; b += blockDim.x) hist[b] = 0;
+      __syncthreads();
+      for (int i = threadIdx.x; i < n; i += blockDim.x) {
+        const unsigned key = __float_as_uint(x[i]);
+        if ((key & mask) == prefix) atomicAdd(&hist[(key >> shift) & 255u], 1u);
+      }
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        unsigned cum = 0;
+        int b = 255;
+        for (; b > 0; --b) {
+          if (cum + hist[b] >= remaining) break;
+          cum += hist[b];
+        }
+        s_prefix = prefix | ((unsigned)b << shift);
+        s_remaining = remaining - cum;
+      }
+      __syncthreads();
+      prefix = s_prefix;
+      remaining = s_remaining;
+      mask |= 255u << shift;
+      __syncthreads();
+    }
+  }
+  // prefix = bits of the k-th largest value T; keep x > T, and the first `remaining` x == T
+  unsigned eq_before = 0;                                   // equal values in earlier chunks
+  for (int c0 = 0; c0 < W * 32; c0 += blockDim.x) {
+    const int i = c0 + threadIdx.x;
+    const unsigned key = i < n ? __float_as_uint(x[i]) : 0u;
+    const bool eq = !all && i < n && key == prefix;
+    const unsigned eb = __ballot_sync(0xffffffffu, eq);
+    if (lane == 0) s_warp[warp] = __popc(eb);
+    __syncthreads();
+    unsigned before = eq_before;
+    unsigned tot = 0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) {
+      if (w < warp) before += s_warp[w];
+      tot += s_warp[w];
+    }
+    before += __popc(eb & ((1u << lane) - 1u));
+    bool sel = i < n && (all || key > prefix || (eq && before < remaining));
+    sel = sel || (i < n_sink);
+    const unsigned word = __ballot_sync(0xffffffffu, sel);
+    if (lane == 0 && (i >> 5) < W) out[row * W + (i >> 5)] = word;
+    eq_before += tot;
+    __syncthreads();
+  }
+}
+
+// Token-level M_{S->K} (READING 14): one CTA per (b,h, target query block g_K).
+// Every selected token of source block phi(g_K) is projected by Decompose-Align-Project with the
+// forward-interval footprint (mark_image at block size 1, i.e. token granularity), then the sink
+// tokens j < C_sink are added.
+__global__ void map_tokens_kernel(const Geo g, int S, int K, int C, int sink_scales, int mode,
+                                  const uint32_t* __restrict__ src, uint32_t* __restrict__ dst) {
+  extern __shared__ uint32_t trow[];
+  const int G_S = (g.side[S - 1] * g.side[S - 1] + C - 1) / C;
+  const int G_K = (g.side[K - 1] * g.side[K - 1] + C - 1) / C;
+  const int bh = blockIdx.x / G_K, gk = blockIdx.x % G_K;
+  const int n_S = g.cum[S], n_K = g.cum[K];
+  const int W_S = (n_S + 31) / 32, W_K = (n_K + 31) / 32;
+  for (int w = threadIdx.x; w < W_K; w += blockDim.x) trow[w] = 0;
+  __syncthreads();
+  // phi(g_K) = clamp(rne(((2 g_K + 1) G_S - G_K) / (2 G_K)), 0, G_S - 1)
+  const int gs = min(max(rne_div((long long)(2 * gk + 1) * G_S - G_K, 2LL * G_K), 0), G_S - 1);
+  const uint32_t* srow = src + ((long long)bh * G_S + gs) * W_S;
+  for (int j = threadIdx.x; j < n_S; j += blockDim.x)
+    if ((__ldg(srow + (j >> 5)) >> (j & 31)) & 1u) mark_image(g, j, K - S, mode, 1, trow);
+  if (threadIdx.x == 0 && sink_scales > 0) set_bit_range(trow, 0, g.cum[sink_scales] - 1);
+  __syncthreads();
+  uint32_t* drow = dst + ((long long)bh * G_K + gk) * W_K;
+  for (int w = threadIdx.x; w < W_K; w += blockDim.x) drow[w] = trow[w];
+}
+
 // ------------------------------------------------------------------------------------ a5
 // Up to 32 CTAs, each owning a contiguous range of rows.  A CTA first counts the set bits of all
 // rows before its range (coalesced over words; at most a few thousand L2 hits) to get its base
@@ -410,6 +506,24 @@ cudaError_t launch_build_lists(int bh, int g_q, int g_kv, const MaskSet& ms, int
   ctas = (rows + per - 1) / per;
   build_lists_kernel<<<ctas, BL_THREADS, 0, st>>>(rows, g_q, g_kv, ms, row_ptr, col_idx, cap, status,
                                                   per);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_topk_tokens(int rows, int n, int k_tok, int n_sink, const float* a,
+                               uint32_t* out, cudaStream_t st) {
+  if (rows <= 0) return cudaSuccess;
+  topk_tokens_kernel<<<rows, TK_THREADS, 0, st>>>(a, n, k_tok, n_sink, out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_map_tokens(const Geo& g, int S, int K, int C, int sink_scales, int mode,
+                              int bh, const uint32_t* src, uint32_t* dst, cudaStream_t st) {
+  const int G_K = (g.side[K - 1] * g.side[K - 1] + C - 1) / C;
+  const size_t shm = size_t((g.cum[K] + 31) / 32) * 4;
+  if (shm > 48 * 1024) return cudaErrorInvalidValue;
+  const long long grid = (long long)bh * G_K;
+  if (grid <= 0) return cudaSuccess;
+  map_tokens_kernel<<<(unsigned)grid, 256, shm, st>>>(g, S, K, C, sink_scales, mode, src, dst);
   return cudaGetLastError();
 }
 

@@ -1,0 +1,378 @@
+// token.cu — NEXT(2), token-granular CS4A (the paper's own CS4A granularity) for sm_100a.
+//
+//  * colsum_kernel: A^(S)[g, j] = sum_{q in query block g} P[q, j]
+//    over query blocks of C rows.  Computed transposed, S^T = K Q_g^T (tcgen05, M = 128 keys,
+//    N = C queries, accumulator in TMEM), so each thread owns one key row and the column sum of
+//    P is the row sum sum_q 2^(s_jq * scale * log2 e - L_q) with L_q = lse_q * log2 e taken from
+//    the decision scale's dense pass: no cross-thread reduction, fp32 throughout.
+//  * token_attn_kernel: Delta O^(K) over per-query-block token lists (PAPER.md:318-328,
+//    824-830 "gathers discrete, non-contiguous key and value vectors ... packed into contiguous
+//    dense tiles within shared memory"): a producer warp gathers 128 listed K and V rows per
+//    chunk with cp.async straight into the 128-byte-swizzled layout the tensor core reads,
+//    tcgen05 computes S = Q K^T and O += P V with S / P / O in TMEM, and one softmax thread per
+//    query row runs the fp32 online softmax (exp2 domain, lazy rescale).  One CTA per
+//    (b,h, query block, 128-row sub-tile), chunks in sequence; two CTAs share an SM.
+#include <cuda_bf16.h>
+#include <cstdio>
+
+#include "kernels.h"
+#include "ptx.cuh"
+#include "kernel_util.cuh"
+
+namespace sv {
+namespace {
+
+constexpr int TBM = 128;           // key rows per colsum tile / query rows per attention tile
+
+// ------------------------------------------------------------------------------- column sums
+template <int D, int C>
+struct ColCfg {
+  static constexpr int NBOX = D / 64;
+  static constexpr int K_BYTES = TBM * D * 2;
+  static constexpr int Q_BYTES = C * D * 2;
+  static constexpr int SMEM = K_BYTES + Q_BYTES + C * 4 + 1024;   // + alignment slack
+};
+
+template <int D, int C>
+__global__ void __launch_bounds__(128) colsum_kernel(const __grid_constant__ CUtensorMap tmap_k,
+                                                     const __grid_constant__ CUtensorMap tmap_q,
+                                                     int n_q, int n_kv, int G, float scale_log2,
+                                                     const float* __restrict__ lse,
+                                                     float* __restrict__ out) {
+  using CF = ColCfg<D, C>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~uintptr_t(1023));       // SW128 tiles: 1 KB aligned
+  uint8_t* sK = smem;
+  uint8_t* sQ = smem + CF::K_BYTES;
+  float* sL = reinterpret_cast<float*>(sQ + CF::Q_BYTES);
+  __shared__ uint64_t bar_load, bar_mma;
+  __shared__ uint32_t tslot;
+  const int kt = blockIdx.x, g = blockIdx.y, bh = blockIdx.z;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    mbar_init(&bar_load, 1);
+    mbar_init(&bar_mma, 1);
+    fence_barrier_init();
+  }
+  if (warp == 0) {
+    tmem_alloc(&tslot, 256);
+    tmem_relinquish();
+  }
+  // L_q of the block's queries; rows past N_S contribute 2^-inf = 0
+  for (int c = threadIdx.x; c < C; c += blockDim.x) {
+    const int q = g * C + c;
+    sL[c] = q < n_q ? lse[(long long)bh * n_q + q] * 1.4426950408889634f : INFINITY;
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = tslot;
+  if (threadIdx.x == 0) {
+    mbar_arrive_expect_tx(&bar_load, CF::K_BYTES + CF::Q_BYTES);
+#pragma unroll
+    for (int b = 0; b < CF::NBOX; ++b) {
+      tma_load_3d(sK + b * (TBM * 128), &tmap_k, &bar_load, b * 64, kt * TBM, bh);
+      tma_load_3d(sQ + b * (C * 128), &tmap_q, &bar_load, b * 64, g * C, bh);
+    }
+  }
+  if (warp == 0) {
+    mbar_wait(&bar_load, 0);
+    tc_fence_after();
+    if (elect_one()) {
+      constexpr uint32_t IDESC = idesc_bf16_f32(TBM, C, 0, 0);
+      const uint64_t da = sdesc_sw128(smem_u32(sK), 16, 1024);
+      const uint64_t db = sdesc_sw128(smem_u32(sQ), 16, 1024);
+#pragma unroll
+      for (int kk = 0; kk < D / 16; ++kk) {
+        const uint32_t oa = ((kk >> 2) * (TBM * 128) + (kk & 3) * 32) >> 4;
+        const uint32_t ob = ((kk >> 2) * (C * 128) + (kk & 3) * 32) >> 4;
+        mma_ss(tmem, da + oa, db + ob, IDESC, kk > 0);
+      }
+      mma_commit(&bar_mma);
+    }
+    __syncwarp();
+  }
+  mbar_wait(&bar_mma, 0);
+  tc_fence_after();
+  const uint32_t t_row = tmem + (uint32_t(warp * 32) << 16);
+  float acc = 0.f;
+#pragma unroll 1
+  for (int c0 = 0; c0 < C; c0 += 32) {
+    uint32_t s[32];
+    tmem_ld32(t_row + c0, s);
+    tmem_wait_ld();
+#pragma unroll
+    for (int i = 0; i < 32; ++i) acc += ex2(__uint_as_float(s[i]) * scale_log2 - sL[c0 + i]);
+  }
+  const int j = kt * TBM + warp * 32 + lane;
+  if (j < n_kv) out[((long long)bh * G + g) * n_kv + j] = acc;
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) {
+    tc_fence_after();
+    tmem_dealloc(tmem, 256);
+  }
+}
+
+// ------------------------------------------------------------------------ token-list attention
+template <int D>
+struct TokCfg {
+  static constexpr int NBOX = D / 64;
+  static constexpr int TILE_BYTES = TBM * D * 2;
+  static constexpr int SMEM = 3 * TILE_BYTES + 1024;    // Q, K chunk, V chunk (+ alignment)
+};
+
+__device__ __forceinline__ void cp_async16(uint32_t dst, const void* src, bool valid) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src),
+               "r"(valid ? 16 : 0)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() {
+  asm volatile("cp.async.wait_all;" ::: "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
+// one CTA per (b,h, query block g, 128-row sub-tile); warps 0-3 softmax (one query row each),
+// warp 4 gathers and issues the MMAs
+template <int D>
+__global__ void __launch_bounds__(160) token_attn_kernel(const __grid_constant__ CUtensorMap tmap_q,
+                                                         const uint16_t* __restrict__ k,
+                                                         const uint16_t* __restrict__ v,
+                                                         long long kv_stride, int n_q, int C,
+                                                         int G, int subs, float scale_log2,
+                                                         const int* __restrict__ row_ptr,
+                                                         const int* __restrict__ col_idx,
+                                                         uint16_t* __restrict__ o,
+                                                         long long o_stride) {
+  using TC = TokCfg<D>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~uintptr_t(1023));
+  uint8_t* sQ = smem;
+  uint8_t* sK = smem + TC::TILE_BYTES;
+  uint8_t* sV = smem + 2 * TC::TILE_BYTES;
+  __shared__ uint64_t q_full, s_bar, p_bar, pv_bar;
+  __shared__ uint32_t tslot;
+  const int item = blockIdx.x;
+  const int sub = item % subs, g = (item / subs) % G, bh = item / (subs * G);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int r = bh * G + g;
+  const int beg = __ldg(row_ptr + r), n = __ldg(row_ptr + r + 1) - beg;
+  const int chunks = (n + TBM - 1) / TBM;
+  const int row0 = g * C + sub * TBM;                       // first query row of this tile
+  const int row_end = min(g * C + C, n_q);                  // rows of block g
+  if (threadIdx.x == 0) {
+    mbar_init(&q_full, 1);
+    mbar_init(&s_bar, 1);
+    mbar_init(&p_bar, TBM);
+    mbar_init(&pv_bar, 1);
+    fence_barrier_init();
+  }
+  if (warp == 4) {
+    tmem_alloc(&tslot, 256);
+    tmem_relinquish();
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = tslot;                              // S/P: cols [0,128), O: [128, 128+D)
+  if (warp == 4) {
+    // ------------------------------------------------------------ gather + tcgen05 issue
+    if (lane == 0) {
+      mbar_arrive_expect_tx(&q_full, TC::TILE_BYTES);
+#pragma unroll
+      for (int b = 0; b < TC::NBOX; ++b)
+        tma_load_3d(sQ + b * (TBM * 128), &tmap_q, &q_full, b * 64, row0, bh);
+    }
+    constexpr uint32_t IDESC_QK = idesc_bf16_f32(TBM, TBM, 0, 0);
+    constexpr uint32_t IDESC_PV = idesc_bf16_f32(TBM, D, 0, 1);
+    const uint64_t dq = sdesc_sw128(smem_u32(sQ), 16, 1024);
+    const uint64_t dk = sdesc_sw128(smem_u32(sK), 16, 1024);
+    const uint64_t dv = sdesc_sw128(smem_u32(sV), TBM * 128, 1024);
+    const uint16_t* kb = k + (long long)bh * kv_stride;
+    const uint16_t* vb = v + (long long)bh * kv_stride;
+    if (chunks == 0) mbar_wait(&q_full, 0);                // no TMA in flight at exit
+    for (int c = 0; c < chunks; ++c) {
+      if (c > 0) mbar_wait(&pv_bar, (c - 1) & 1);          // K, V buffers free, O up to date
+      // packed gather: list entries c*128 + i -> smem row i, 16-byte pieces in the SW128 order
+      for (int i = lane; i < TBM; i += 32) {
+        const int e = c * TBM + i;
+        const bool ok = e < n;
+        const int tok = ok ? __ldg(col_idx + beg + e) : 0;
+        const uint16_t* ks = kb + (long long)tok * D;
+        const uint16_t* vs = vb + (long long)tok * D;
+#pragma unroll
+        for (int p = 0; p < D / 8; ++p) {
+          const uint32_t off = (p >> 3) * (TBM * 128) + i * 128 + (((p & 7) ^ (i & 7)) << 4);
+          cp_async16(smem_u32(sK) + off, ks + p * 8, ok);
+          cp_async16(smem_u32(sV) + off, vs + p * 8, ok);
+        }
+      }
+      cp_async_wait_all();
+      fence_proxy_async();
+      __syncwarp();
+      if (c == 0) mbar_wait(&q_full, 0);
+      tc_fence_after();
+      if (elect_one()) {
+#pragma unroll
+        for (int kk = 0; kk < D / 16; ++kk) {
+          const uint32_t oa = ((kk >> 2) * (TBM * 128) + (kk & 3) * 32) >> 4;
+          mma_ss(tmem, dq + oa, dk + oa, IDESC_QK, kk > 0);
+        }
+        mma_commit(&s_bar);
+      }
+      __syncwarp();
+      mbar_wait(&p_bar, c & 1);
+      tc_fence_after();
+      if (elect_one()) {
+#pragma unroll
+        for (int kk = 0; kk < TBM / 16; ++kk)
+          mma_ts(tmem + 128, tmem + kk * 8, dv + ((uint32_t)(kk * 2048) >> 4), IDESC_PV,
+                 (c > 0 || kk > 0) ? 1u : 0u);
+        mma_commit(&pv_bar);
+      }
+      __syncwarp();
+    }
+  } else {
+    // ------------------------------------------------------------ softmax, one row per thread
+    const int row = warp * 32 + lane;
+    const uint32_t t_row = tmem + (uint32_t(warp * 32) << 16);
+    float m = -INFINITY, l = 0.f;
+    for (int c = 0; c < chunks; ++c) {
+      mbar_wait(&s_bar, c & 1);
+      tc_fence_after();
+      uint32_t s[TBM];
+#pragma unroll
+      for (int c0 = 0; c0 < TBM; c0 += 32) tmem_ld32(t_row + c0, s + c0);
+      tmem_wait_ld();
+      const int valid = min(TBM, n - c * TBM);
+      if (valid < TBM) {
+#pragma unroll
+        for (int i = 0; i < TBM; ++i)
+          if (i >= valid) s[i] = __float_as_uint(-INFINITY);
+      }
+      float mx = -INFINITY;
+#pragma unroll
+      for (int i = 0; i < TBM; i += 2) mx = fmax3(mx, __uint_as_float(s[i]), __uint_as_float(s[i + 1]));
+      const float mx_s = mx * scale_log2;
+      if (mx_s > m + 8.0f) {
+        // P_{c-1} V is complete: the producer waited for it before gathering chunk c
+        const float alpha = ex2(m - mx_s);
+        l *= alpha;
+        m = mx_s;
+        if (c > 0) {
+#pragma unroll 1
+          for (int c0 = 0; c0 < D; c0 += 32) {
+            uint32_t ov[32];
+            tmem_ld32(t_row + 128 + c0, ov);
+            tmem_wait_ld();
+#pragma unroll
+            for (int i = 0; i < 32; ++i) ov[i] = __float_as_uint(__uint_as_float(ov[i]) * alpha);
+            tmem_st32(t_row + 128 + c0, ov);
+          }
+        }
+      }
+      const float mref = (m == -INFINITY) ? 0.f : m;
+      float sum = 0.f;
+#pragma unroll
+      for (int c0 = 0; c0 < TBM; c0 += 32) {
+        uint32_t pk[16];
+#pragma unroll
+        for (int i = 0; i < 32; i += 2) {
+          const float p0 = ex2(__uint_as_float(s[c0 + i]) * scale_log2 - mref);
+          const float p1 = ex2(__uint_as_float(s[c0 + i + 1]) * scale_log2 - mref);
+          sum += p0 + p1;
+          pk[i / 2] = pack_bf16x2(p0, p1);
+        }
+        tmem_st16(t_row + c0 / 2, pk);
+      }
+      l += sum;
+      tmem_wait_st();
+      tc_fence_before();
+      mbar_arrive(&p_bar);
+    }
+    // epilogue: O / l -> bf16 rows of this query block
+    const int q = row0 + row;
+    const bool store = q < row_end && sub * TBM + row < C;
+    uint16_t* orow = o + (long long)bh * o_stride + (long long)q * D;
+    if (chunks > 0) {
+      mbar_wait(&pv_bar, (chunks - 1) & 1);
+      tc_fence_after();
+      const float inv = 1.f / l;
+#pragma unroll 1
+      for (int c0 = 0; c0 < D; c0 += 16) {
+        uint32_t ov[16];
+        tmem_ld16(t_row + 128 + c0, ov);
+        tmem_wait_ld();
+        uint32_t pk[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i)
+          pk[i] = pack_bf16x2(__uint_as_float(ov[2 * i]) * inv, __uint_as_float(ov[2 * i + 1]) * inv);
+        if (store) {
+          uint4* dst = reinterpret_cast<uint4*>(orow + c0);
+          dst[0] = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+          dst[1] = make_uint4(pk[4], pk[5], pk[6], pk[7]);
+        }
+      }
+    } else if (store) {
+      for (int c0 = 0; c0 < D; c0 += 8) *reinterpret_cast<uint4*>(orow + c0) = make_uint4(0, 0, 0, 0);
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 4) {
+    tc_fence_after();
+    tmem_dealloc(tmem, 256);
+  }
+}
+
+}  // namespace
+
+cudaError_t launch_colsum(int head_dim, int C, const CUtensorMap& tk, const CUtensorMap& tq,
+                          int bh, int n_q, int n_kv, float scale_log2, const float* lse,
+                          float* out, cudaStream_t st) {
+  const int G = (n_q + C - 1) / C;
+  const dim3 grid((n_kv + TBM - 1) / TBM, G, bh);
+#define SV_COL(D_, C_)                                                                       \
+  if (head_dim == D_ && C == C_) {                                                           \
+    auto kern = colsum_kernel<D_, C_>;                                                       \
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,   \
+                                         ColCfg<D_, C_>::SMEM);                              \
+    if (e != cudaSuccess) return e;                                                          \
+    kern<<<grid, 128, ColCfg<D_, C_>::SMEM, st>>>(tk, tq, n_q, n_kv, G, scale_log2, lse, out); \
+    return cudaGetLastError();                                                               \
+  }
+  SV_COL(128, 192) SV_COL(128, 128) SV_COL(128, 64) SV_COL(64, 192) SV_COL(64, 128) SV_COL(64, 64)
+#undef SV_COL
+  return cudaErrorInvalidValue;
+}
+
+cudaError_t launch_token_attn(int head_dim, const CUtensorMap& tq, const uint16_t* k,
+                              const uint16_t* v, long long kv_stride, int bh, int n_q, int C,
+                              float scale_log2, const int* row_ptr, const int* col_idx,
+                              uint16_t* o, long long o_stride, cudaStream_t st) {
+  const int G = (n_q + C - 1) / C;
+  const int subs = (C + TBM - 1) / TBM;
+  const long long items = (long long)bh * G * subs;
+  if (items <= 0) return cudaSuccess;
+  if (items > (1LL << 31) - 1) return cudaErrorInvalidValue;
+#define SV_TOK(D_)                                                                            \
+  if (head_dim == D_) {                                                                       \
+    auto kern = token_attn_kernel<D_>;                                                        \
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,    \
+                                         TokCfg<D_>::SMEM);                                   \
+    if (e != cudaSuccess) return e;                                                           \
+    kern<<<(unsigned)items, 160, TokCfg<D_>::SMEM, st>>>(tq, k, v, kv_stride, n_q, C, G, subs, \
+                                                          scale_log2, row_ptr, col_idx, o,     \
+                                                          o_stride);                          \
+    return cudaGetLastError();                                                                \
+  }
+  SV_TOK(128) SV_TOK(64)
+#undef SV_TOK
+  return cudaErrorInvalidValue;
+}
+
+}  // namespace sv
