@@ -436,6 +436,93 @@ __global__ void __launch_bounds__(BL_THREADS) build_lists_kernel(int rows, int g
   if (err && status) atomicCAS(status, 0, err);
 }
 
+// Wide rows (W > BL_WMAX words, e.g. token bit rows of NEXT(2)): three passes instead of one
+// kernel that re-counts every earlier row.  (1) one warp per row writes its popcount (OR of the
+// masks) to row_ptr[r + 1]; (2) one CTA scans row_ptr in place (chunked, deterministic) and
+// flags empty rows / capacity; (3) one CTA per row writes the ascending column list, a block
+// scan of the per-word counts giving each word's offset.
+__global__ void __launch_bounds__(256) wide_count_kernel(int rows, int g_q, int W, MaskSet ms,
+                                                         int* __restrict__ row_ptr) {
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (warp >= rows) return;
+  int c = 0;
+  for (int w = lane; w < W; w += 32) c += __popc(row_word(ms, warp, warp % g_q, w, W));
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+  if (lane == 0) row_ptr[warp + 1] = c;
+}
+
+__global__ void __launch_bounds__(1024) wide_scan_kernel(int rows, int* __restrict__ row_ptr,
+                                                         long long cap, int* status) {
+  __shared__ int s_warp[32];
+  __shared__ long long s_carry;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) { s_carry = 0; row_ptr[0] = 0; }
+  __syncthreads();
+  int err = 0;
+  for (int c0 = 0; c0 < rows; c0 += blockDim.x) {
+    const int r = c0 + threadIdx.x;
+    const int c = r < rows ? row_ptr[r + 1] : 0;
+    if (r < rows && c == 0) err = 5;                        // SPARVAR_ERR_EMPTY_ROW
+    int inc = c;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int t = __shfl_up_sync(0xffffffffu, inc, o);
+      if (lane >= o) inc += t;
+    }
+    if (lane == 31) s_warp[warp] = inc;
+    __syncthreads();
+    int wpre = 0, tot = 0;
+    for (int i = 0; i < (int)(blockDim.x >> 5); ++i) {
+      if (i < warp) wpre += s_warp[i];
+      tot += s_warp[i];
+    }
+    const long long carry = s_carry;
+    if (r < rows) row_ptr[r + 1] = (int)(carry + wpre + inc);
+    __syncthreads();
+    if (threadIdx.x == 0) s_carry = carry + tot;
+    __syncthreads();
+  }
+  if (s_carry > cap && threadIdx.x == 0 && status) atomicCAS(status, 0, 4);   // CAPACITY
+  if (err && status) atomicCAS(status, 0, err);
+}
+
+__global__ void __launch_bounds__(256) wide_write_kernel(int g_q, int W, MaskSet ms,
+                                                         const int* __restrict__ row_ptr,
+                                                         int* __restrict__ col_idx, long long cap) {
+  __shared__ int s_warp[8];
+  __shared__ int s_carry;
+  const int r = blockIdx.x;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const long long base = row_ptr[r];
+  if ((long long)row_ptr[r + 1] > cap) return;             // capacity error already flagged
+  if (threadIdx.x == 0) s_carry = 0;
+  __syncthreads();
+  for (int w0 = 0; w0 < W; w0 += blockDim.x) {
+    const int w = w0 + threadIdx.x;
+    const uint32_t x = w < W ? row_word(ms, r, r % g_q, w, W) : 0u;
+    const int c = __popc(x);
+    int inc = c;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int t = __shfl_up_sync(0xffffffffu, inc, o);
+      if (lane >= o) inc += t;
+    }
+    if (lane == 31) s_warp[warp] = inc;
+    __syncthreads();
+    int wpre = 0, tot = 0;
+    for (int i = 0; i < (int)(blockDim.x >> 5); ++i) {
+      if (i < warp) wpre += s_warp[i];
+      tot += s_warp[i];
+    }
+    long long pos = base + s_carry + wpre + inc - c;
+    for (uint32_t y = x; y; y &= y - 1) col_idx[pos++] = w * 32 + __ffs(y) - 1;
+    __syncthreads();
+    if (threadIdx.x == 0) s_carry += tot;
+    __syncthreads();
+  }
+}
+
 }  // namespace
 
 cudaError_t launch_local_mask(const Geo& g, int target, int block, int sink_scales,
@@ -500,6 +587,13 @@ cudaError_t launch_map_indices(const Geo& g, int S, int K, int block, int sink_s
 cudaError_t launch_build_lists(int bh, int g_q, int g_kv, const MaskSet& ms, int* row_ptr,
                                int* col_idx, long long cap, int* status, cudaStream_t st) {
   const int rows = bh * g_q;
+  const int W = (g_kv + 31) / 32;
+  if (W > BL_WMAX) {
+    wide_count_kernel<<<(rows * 32 + 255) / 256, 256, 0, st>>>(rows, g_q, W, ms, row_ptr);
+    wide_scan_kernel<<<1, 1024, 0, st>>>(rows, row_ptr, cap, status);
+    wide_write_kernel<<<rows, 256, 0, st>>>(g_q, W, ms, row_ptr, col_idx, cap);
+    return cudaGetLastError();
+  }
   int ctas = (rows + 63) / 64;
   if (ctas > BL_MAX_CTAS) ctas = BL_MAX_CTAS;
   const int per = (rows + ctas - 1) / ctas;

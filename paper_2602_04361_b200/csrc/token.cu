@@ -11,7 +11,7 @@
 //    chunk with cp.async straight into the 128-byte-swizzled layout the tensor core reads,
 //    tcgen05 computes S = Q K^T and O += P V with S / P / O in TMEM, and one softmax thread per
 //    query row runs the fp32 online softmax (exp2 domain, lazy rescale).  One CTA per
-//    (b,h, query block, 128-row sub-tile), chunks in sequence; two CTAs share an SM.
+//    (b,h, query block, 128-row sub-tile); four gather warps fill double-buffered K/V chunks.
 #include <cuda_bf16.h>
 #include <cstdio>
 
@@ -120,7 +120,7 @@ template <int D>
 struct TokCfg {
   static constexpr int NBOX = D / 64;
   static constexpr int TILE_BYTES = TBM * D * 2;
-  static constexpr int SMEM = 3 * TILE_BYTES + 1024;    // Q, K chunk, V chunk (+ alignment)
+  static constexpr int SMEM = 5 * TILE_BYTES + 1024;    // Q, 2 K chunks, 2 V chunks (+ alignment)
 };
 
 __device__ __forceinline__ void cp_async16(uint32_t dst, const void* src, bool valid) {
@@ -135,26 +135,28 @@ __device__ __forceinline__ void fence_proxy_async() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
 
-// one CTA per (b,h, query block g, 128-row sub-tile); warps 0-3 softmax (one query row each),
-// warp 4 gathers and issues the MMAs
+// one CTA per (b,h, query block g, 128-row sub-tile).  Warps 0-3: softmax (one query row per
+// thread) and epilogue; warp 4: tcgen05 issue; warps 5-8: gather.  K/V chunks are double
+// buffered, so the gather of chunk c+1 runs under the softmax of chunk c.  Issue order per chunk
+// c >= 1: O += P_{c-1} V_{c-1}, then S = Q K_c^T (S/P alias in TMEM: the tensor pipe runs them
+// in order, and S_c complete implies P_{c-1} V_{c-1} complete for the softmax's O rescale).
+constexpr int TOK_GATHER_WARPS = 4;
+constexpr int TOK_THREADS = (5 + TOK_GATHER_WARPS) * 32;
+
 template <int D>
-__global__ void __launch_bounds__(160) token_attn_kernel(const __grid_constant__ CUtensorMap tmap_q,
-                                                         const uint16_t* __restrict__ k,
-                                                         const uint16_t* __restrict__ v,
-                                                         long long kv_stride, int n_q, int C,
-                                                         int G, int subs, float scale_log2,
-                                                         const int* __restrict__ row_ptr,
-                                                         const int* __restrict__ col_idx,
-                                                         uint16_t* __restrict__ o,
-                                                         long long o_stride) {
+__global__ void __launch_bounds__(TOK_THREADS, 1) token_attn_kernel(
+    const __grid_constant__ CUtensorMap tmap_q, const uint16_t* __restrict__ k,
+    const uint16_t* __restrict__ v, long long kv_stride, int n_q, int C, int G, int subs,
+    float scale_log2, const int* __restrict__ row_ptr, const int* __restrict__ col_idx,
+    uint16_t* __restrict__ o, long long o_stride) {
   using TC = TokCfg<D>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~uintptr_t(1023));
   uint8_t* sQ = smem;
-  uint8_t* sK = smem + TC::TILE_BYTES;
-  uint8_t* sV = smem + 2 * TC::TILE_BYTES;
-  __shared__ uint64_t q_full, s_bar, p_bar, pv_bar;
+  uint8_t* sK = smem + TC::TILE_BYTES;                      // [2] chunk buffers
+  uint8_t* sV = smem + 3 * TC::TILE_BYTES;                  // [2]
+  __shared__ uint64_t q_full, s_bar, p_bar, pv_done, kv_full[2], kv_empty[2];
   __shared__ uint32_t tslot;
   const int item = blockIdx.x;
   const int sub = item % subs, g = (item / subs) % G, bh = item / (subs * G);
@@ -168,7 +170,11 @@ __global__ void __launch_bounds__(160) token_attn_kernel(const __grid_constant__
     mbar_init(&q_full, 1);
     mbar_init(&s_bar, 1);
     mbar_init(&p_bar, TBM);
-    mbar_init(&pv_bar, 1);
+    mbar_init(&pv_done, 1);
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&kv_full[b], TOK_GATHER_WARPS);
+      mbar_init(&kv_empty[b], 1);
+    }
     fence_barrier_init();
   }
   if (warp == 4) {
@@ -179,8 +185,37 @@ __global__ void __launch_bounds__(160) token_attn_kernel(const __grid_constant__
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = tslot;                              // S/P: cols [0,128), O: [128, 128+D)
-  if (warp == 4) {
-    // ------------------------------------------------------------ gather + tcgen05 issue
+  if (warp >= 5) {
+    // ------------------------------------------------------------ packed gather (cp.async)
+    // list entry c*128 + i -> row i of buffer c&1, 16-byte pieces in the SW128 order the tensor
+    // core reads; rows past the list are zero-filled (their logits are masked to -inf)
+    const int gw = warp - 5;
+    const uint16_t* kb = k + (long long)bh * kv_stride;
+    const uint16_t* vb = v + (long long)bh * kv_stride;
+    for (int c = 0; c < chunks; ++c) {
+      const int b = c & 1;
+      if (c >= 2) mbar_wait(&kv_empty[b], ((c >> 1) - 1) & 1);
+      const uint32_t dK = smem_u32(sK + b * TC::TILE_BYTES), dV = smem_u32(sV + b * TC::TILE_BYTES);
+      for (int i = gw * 32 + lane; i < TBM; i += TOK_GATHER_WARPS * 32) {
+        const int e = c * TBM + i;
+        const bool ok = e < n;
+        const int tok = ok ? __ldg(col_idx + beg + e) : 0;
+        const uint16_t* ks = kb + (long long)tok * D;
+        const uint16_t* vs = vb + (long long)tok * D;
+#pragma unroll
+        for (int p = 0; p < D / 8; ++p) {
+          const uint32_t off = (p >> 3) * (TBM * 128) + i * 128 + (((p & 7) ^ (i & 7)) << 4);
+          cp_async16(dK + off, ks + p * 8, ok);
+          cp_async16(dV + off, vs + p * 8, ok);
+        }
+      }
+      cp_async_wait_all();
+      fence_proxy_async();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&kv_full[b]);
+    }
+  } else if (warp == 4) {
+    // ------------------------------------------------------------ tcgen05 issue
     if (lane == 0) {
       mbar_arrive_expect_tx(&q_full, TC::TILE_BYTES);
 #pragma unroll
@@ -190,32 +225,28 @@ __global__ void __launch_bounds__(160) token_attn_kernel(const __grid_constant__
     constexpr uint32_t IDESC_QK = idesc_bf16_f32(TBM, TBM, 0, 0);
     constexpr uint32_t IDESC_PV = idesc_bf16_f32(TBM, D, 0, 1);
     const uint64_t dq = sdesc_sw128(smem_u32(sQ), 16, 1024);
-    const uint64_t dk = sdesc_sw128(smem_u32(sK), 16, 1024);
-    const uint64_t dv = sdesc_sw128(smem_u32(sV), TBM * 128, 1024);
-    const uint16_t* kb = k + (long long)bh * kv_stride;
-    const uint16_t* vb = v + (long long)bh * kv_stride;
-    if (chunks == 0) mbar_wait(&q_full, 0);                // no TMA in flight at exit
-    for (int c = 0; c < chunks; ++c) {
-      if (c > 0) mbar_wait(&pv_bar, (c - 1) & 1);          // K, V buffers free, O up to date
-      // packed gather: list entries c*128 + i -> smem row i, 16-byte pieces in the SW128 order
-      for (int i = lane; i < TBM; i += 32) {
-        const int e = c * TBM + i;
-        const bool ok = e < n;
-        const int tok = ok ? __ldg(col_idx + beg + e) : 0;
-        const uint16_t* ks = kb + (long long)tok * D;
-        const uint16_t* vs = vb + (long long)tok * D;
-#pragma unroll
-        for (int p = 0; p < D / 8; ++p) {
-          const uint32_t off = (p >> 3) * (TBM * 128) + i * 128 + (((p & 7) ^ (i & 7)) << 4);
-          cp_async16(smem_u32(sK) + off, ks + p * 8, ok);
-          cp_async16(smem_u32(sV) + off, vs + p * 8, ok);
-        }
-      }
-      cp_async_wait_all();
-      fence_proxy_async();
-      __syncwarp();
-      if (c == 0) mbar_wait(&q_full, 0);
+    mbar_wait(&q_full, 0);
+    auto pv = [&](int c) {                                  // O += P_c V_c
+      mbar_wait(&p_bar, c & 1);
       tc_fence_after();
+      const int b = c & 1;
+      const uint64_t dv = sdesc_sw128(smem_u32(sV + b * TC::TILE_BYTES), TBM * 128, 1024);
+      if (elect_one()) {
+#pragma unroll
+        for (int kk = 0; kk < TBM / 16; ++kk)
+          mma_ts(tmem + 128, tmem + kk * 8, dv + ((uint32_t)(kk * 2048) >> 4), IDESC_PV,
+                 (c > 0 || kk > 0) ? 1u : 0u);
+        mma_commit(&kv_empty[b]);
+        mma_commit(&pv_done);
+      }
+      __syncwarp();
+    };
+    for (int c = 0; c < chunks; ++c) {
+      const int b = c & 1;
+      mbar_wait(&kv_full[b], (c >> 1) & 1);
+      if (c > 0) pv(c - 1);
+      tc_fence_after();
+      const uint64_t dk = sdesc_sw128(smem_u32(sK + b * TC::TILE_BYTES), 16, 1024);
       if (elect_one()) {
 #pragma unroll
         for (int kk = 0; kk < D / 16; ++kk) {
@@ -225,17 +256,8 @@ __global__ void __launch_bounds__(160) token_attn_kernel(const __grid_constant__
         mma_commit(&s_bar);
       }
       __syncwarp();
-      mbar_wait(&p_bar, c & 1);
-      tc_fence_after();
-      if (elect_one()) {
-#pragma unroll
-        for (int kk = 0; kk < TBM / 16; ++kk)
-          mma_ts(tmem + 128, tmem + kk * 8, dv + ((uint32_t)(kk * 2048) >> 4), IDESC_PV,
-                 (c > 0 || kk > 0) ? 1u : 0u);
-        mma_commit(&pv_bar);
-      }
-      __syncwarp();
     }
+    if (chunks > 0) pv(chunks - 1);
   } else {
     // ------------------------------------------------------------ softmax, one row per thread
     const int row = warp * 32 + lane;
@@ -259,7 +281,7 @@ __global__ void __launch_bounds__(160) token_attn_kernel(const __grid_constant__
       for (int i = 0; i < TBM; i += 2) mx = fmax3(mx, __uint_as_float(s[i]), __uint_as_float(s[i + 1]));
       const float mx_s = mx * scale_log2;
       if (mx_s > m + 8.0f) {
-        // P_{c-1} V is complete: the producer waited for it before gathering chunk c
+        // S_c complete => P_{c-1} V_{c-1} complete (issued before it, in order)
         const float alpha = ex2(m - mx_s);
         l *= alpha;
         m = mx_s;
@@ -299,7 +321,7 @@ __global__ void __launch_bounds__(160) token_attn_kernel(const __grid_constant__
     const bool store = q < row_end && sub * TBM + row < C;
     uint16_t* orow = o + (long long)bh * o_stride + (long long)q * D;
     if (chunks > 0) {
-      mbar_wait(&pv_bar, (chunks - 1) & 1);
+      mbar_wait(&pv_done, (chunks - 1) & 1);
       tc_fence_after();
       const float inv = 1.f / l;
 #pragma unroll 1
@@ -365,7 +387,7 @@ cudaError_t launch_token_attn(int head_dim, const CUtensorMap& tq, const uint16_
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,    \
                                          TokCfg<D_>::SMEM);                                   \
     if (e != cudaSuccess) return e;                                                           \
-    kern<<<(unsigned)items, 160, TokCfg<D_>::SMEM, st>>>(tq, k, v, kv_stride, n_q, C, G, subs, \
+    kern<<<(unsigned)items, TOK_THREADS, TokCfg<D_>::SMEM, st>>>(tq, k, v, kv_stride, n_q, C, G, subs, \
                                                           scale_log2, row_ptr, col_idx, o,     \
                                                           o_stride);                          \
     return cudaGetLastError();                                                                \
