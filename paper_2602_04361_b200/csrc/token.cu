@@ -11,7 +11,8 @@
 //    chunk with cp.async straight into the 128-byte-swizzled layout the tensor core reads,
 //    tcgen05 computes S = Q K^T and O += P V with S / P / O in TMEM, and one softmax thread per
 //    query row runs the fp32 online softmax (exp2 domain, lazy rescale).  One CTA per
-//    (b,h, query block, 128-row sub-tile); four gather warps fill double-buffered K/V chunks.
+//    (b,h, query block): the block's 128-row sub-tiles are two slots sharing every gathered
+//    chunk; seven gather warps fill double-buffered K/V chunks.
 #include <cuda_bf16.h>
 #include <cstdio>
 
@@ -120,7 +121,7 @@ template <int D>
 struct TokCfg {
   static constexpr int NBOX = D / 64;
   static constexpr int TILE_BYTES = TBM * D * 2;
-  static constexpr int SMEM = 5 * TILE_BYTES + 1024;    // Q, 2 K chunks, 2 V chunks (+ alignment)
+  static constexpr int SMEM = 6 * TILE_BYTES + 1024;    // 2 Q tiles, 2 K and 2 V chunks (+ align)
 };
 
 __device__ __forceinline__ void cp_async16(uint32_t dst, const void* src, bool valid) {
@@ -135,140 +136,160 @@ __device__ __forceinline__ void fence_proxy_async() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
 
-// one CTA per (b,h, query block g, 128-row sub-tile).  Warps 0-3: softmax (one query row per
-// thread) and epilogue; warp 4: tcgen05 issue; warps 5-8: gather.  K/V chunks are double
-// buffered, so the gather of chunk c+1 runs under the softmax of chunk c.  Issue order per chunk
-// c >= 1: O += P_{c-1} V_{c-1}, then S = Q K_c^T (S/P alias in TMEM: the tensor pipe runs them
-// in order, and S_c complete implies P_{c-1} V_{c-1} complete for the softmax's O rescale).
-constexpr int TOK_GATHER_WARPS = 4;
-constexpr int TOK_THREADS = (5 + TOK_GATHER_WARPS) * 32;
+// One CTA per (b,h, query block g).  The block's rows run as NS = ceil(C / 128) tile slots
+// (C = 192: rows 0-127 and 128-191) that share every gathered K/V chunk.  Warps 0-3 / 4-7:
+// softmax of slot 0 / 1 (one query row per thread) and its epilogue; warp 8: tcgen05 issue;
+// warps 9-15: gather into double-buffered chunks of 128 tokens.  Issue order per chunk c and
+// slot t: O_t += P_t,c-1 V_c-1, then S_t = Q_t K_c^T (S/P alias in TMEM and the tensor pipe runs
+// one thread's ops in order, so S_t,c complete also means P_t,c-1 V_c-1 is, which the softmax
+// needs before an O rescale).  The two slots' softmax chains interleave on the tensor pipe.
+constexpr int TOK_WARPS = 16;
+constexpr int TOK_THREADS = TOK_WARPS * 32;
+constexpr int TOK_WARP_MMA = 8, TOK_WARP_GATHER0 = 9;
+constexpr int TOK_GATHER_WARPS = TOK_WARPS - TOK_WARP_GATHER0;
+constexpr int TOK_REG_SOFTMAX = 184, TOK_REG_OTHER = 72;
+static_assert(8 * (TOK_REG_SOFTMAX - 128) <= 8 * (128 - TOK_REG_OTHER), "register pool");
 
-template <int D>
+template <int D, int NS>
 __global__ void __launch_bounds__(TOK_THREADS, 1) token_attn_kernel(
     const __grid_constant__ CUtensorMap tmap_q, const uint16_t* __restrict__ k,
-    const uint16_t* __restrict__ v, long long kv_stride, int n_q, int C, int G, int subs,
+    const uint16_t* __restrict__ v, long long kv_stride, int n_q, int C, int G,
     float scale_log2, const int* __restrict__ row_ptr, const int* __restrict__ col_idx,
     uint16_t* __restrict__ o, long long o_stride) {
   using TC = TokCfg<D>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~uintptr_t(1023));
-  uint8_t* sQ = smem;
-  uint8_t* sK = smem + TC::TILE_BYTES;                      // [2] chunk buffers
-  uint8_t* sV = smem + 3 * TC::TILE_BYTES;                  // [2]
-  __shared__ uint64_t q_full, s_bar, p_bar, pv_done, kv_full[2], kv_empty[2];
+  uint8_t* sQ = smem;                                       // [NS]
+  uint8_t* sK = smem + 2 * TC::TILE_BYTES;                  // [2] chunk buffers
+  uint8_t* sV = smem + 4 * TC::TILE_BYTES;                  // [2]
+  __shared__ uint64_t q_full, s_bar[2], p_bar[2], pv_done[2], kv_full[2], kv_empty[2];
   __shared__ uint32_t tslot;
-  const int item = blockIdx.x;
-  const int sub = item % subs, g = (item / subs) % G, bh = item / (subs * G);
+  const int g = blockIdx.x % G, bh = blockIdx.x / G;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int r = bh * G + g;
   const int beg = __ldg(row_ptr + r), n = __ldg(row_ptr + r + 1) - beg;
   const int chunks = (n + TBM - 1) / TBM;
-  const int row0 = g * C + sub * TBM;                       // first query row of this tile
   const int row_end = min(g * C + C, n_q);                  // rows of block g
   if (threadIdx.x == 0) {
     mbar_init(&q_full, 1);
-    mbar_init(&s_bar, 1);
-    mbar_init(&p_bar, TBM);
-    mbar_init(&pv_done, 1);
     for (int b = 0; b < 2; ++b) {
+      mbar_init(&s_bar[b], 1);
+      mbar_init(&p_bar[b], TBM);
+      mbar_init(&pv_done[b], 1);
       mbar_init(&kv_full[b], TOK_GATHER_WARPS);
       mbar_init(&kv_empty[b], 1);
     }
     fence_barrier_init();
   }
-  if (warp == 4) {
-    tmem_alloc(&tslot, 256);
+  if (warp == TOK_WARP_MMA) {
+    tmem_alloc(&tslot, 512);
     tmem_relinquish();
   }
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  const uint32_t tmem = tslot;                              // S/P: cols [0,128), O: [128, 128+D)
-  if (warp >= 5) {
-    // ------------------------------------------------------------ packed gather (cp.async)
-    // list entry c*128 + i -> row i of buffer c&1, 16-byte pieces in the SW128 order the tensor
-    // core reads; rows past the list are zero-filled (their logits are masked to -inf)
-    const int gw = warp - 5;
-    const uint16_t* kb = k + (long long)bh * kv_stride;
-    const uint16_t* vb = v + (long long)bh * kv_stride;
-    for (int c = 0; c < chunks; ++c) {
-      const int b = c & 1;
-      if (c >= 2) mbar_wait(&kv_empty[b], ((c >> 1) - 1) & 1);
-      const uint32_t dK = smem_u32(sK + b * TC::TILE_BYTES), dV = smem_u32(sV + b * TC::TILE_BYTES);
-      for (int i = gw * 32 + lane; i < TBM; i += TOK_GATHER_WARPS * 32) {
-        const int e = c * TBM + i;
-        const bool ok = e < n;
-        const int tok = ok ? __ldg(col_idx + beg + e) : 0;
-        const uint16_t* ks = kb + (long long)tok * D;
-        const uint16_t* vs = vb + (long long)tok * D;
+  const uint32_t tmem = tslot;            // slot t: S/P cols [128t, 128t+128), O [256+128t, +D)
+  if (warp >= TOK_WARP_MMA) {
+    reg_dealloc<TOK_REG_OTHER>();
+    if (warp >= TOK_WARP_GATHER0) {
+      // ---------------------------------------------------------- packed gather (cp.async)
+      // list entry c*128 + i -> row i of buffer c&1, 16-byte pieces in the SW128 order the
+      // tensor core reads; rows past the list are zero-filled (their logits are masked)
+      const int gw = warp - TOK_WARP_GATHER0;
+      const uint16_t* kb = k + (long long)bh * kv_stride;
+      const uint16_t* vb = v + (long long)bh * kv_stride;
+      for (int c = 0; c < chunks; ++c) {
+        const int b = c & 1;
+        if (c >= 2) mbar_wait(&kv_empty[b], ((c >> 1) - 1) & 1);
+        const uint32_t dK = smem_u32(sK + b * TC::TILE_BYTES), dV = smem_u32(sV + b * TC::TILE_BYTES);
+        for (int i = gw * 32 + lane; i < TBM; i += TOK_GATHER_WARPS * 32) {
+          const int e = c * TBM + i;
+          const bool ok = e < n;
+          const int tok = ok ? __ldg(col_idx + beg + e) : 0;
+          const uint16_t* ks = kb + (long long)tok * D;
+          const uint16_t* vs = vb + (long long)tok * D;
 #pragma unroll
-        for (int p = 0; p < D / 8; ++p) {
-          const uint32_t off = (p >> 3) * (TBM * 128) + i * 128 + (((p & 7) ^ (i & 7)) << 4);
-          cp_async16(dK + off, ks + p * 8, ok);
-          cp_async16(dV + off, vs + p * 8, ok);
+          for (int p = 0; p < D / 8; ++p) {
+            const uint32_t off = (p >> 3) * (TBM * 128) + i * 128 + (((p & 7) ^ (i & 7)) << 4);
+            cp_async16(dK + off, ks + p * 8, ok);
+            cp_async16(dV + off, vs + p * 8, ok);
+          }
+        }
+        cp_async_wait_all();
+        fence_proxy_async();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&kv_full[b]);
+      }
+    } else {
+      // ---------------------------------------------------------- tcgen05 issue
+      if (lane == 0) {
+        mbar_arrive_expect_tx(&q_full, NS * TC::TILE_BYTES);
+#pragma unroll
+        for (int t = 0; t < NS; ++t)
+#pragma unroll
+          for (int b = 0; b < TC::NBOX; ++b)
+            tma_load_3d(sQ + t * TC::TILE_BYTES + b * (TBM * 128), &tmap_q, &q_full, b * 64,
+                        g * C + t * TBM, bh);
+      }
+      constexpr uint32_t IDESC_QK = idesc_bf16_f32(TBM, TBM, 0, 0);
+      constexpr uint32_t IDESC_PV = idesc_bf16_f32(TBM, D, 0, 1);
+      mbar_wait(&q_full, 0);
+      auto pv = [&](int t, int c) {                         // O_t += P_t,c V_c
+        mbar_wait(&p_bar[t], c & 1);
+        tc_fence_after();
+        const int b = c & 1;
+        const uint64_t dv = sdesc_sw128(smem_u32(sV + b * TC::TILE_BYTES), TBM * 128, 1024);
+        if (elect_one()) {
+#pragma unroll
+          for (int kk = 0; kk < TBM / 16; ++kk)
+            mma_ts(tmem + 256 + t * 128, tmem + t * 128 + kk * 8, dv + ((uint32_t)(kk * 2048) >> 4),
+                   IDESC_PV, (c > 0 || kk > 0) ? 1u : 0u);
+          if (t == NS - 1) mma_commit(&kv_empty[b]);       // last reader of chunk c's buffers
+          mma_commit(&pv_done[t]);
+        }
+        __syncwarp();
+      };
+      auto qk = [&](int t, int c) {                         // S_t = Q_t K_c^T
+        const uint64_t dq = sdesc_sw128(smem_u32(sQ + t * TC::TILE_BYTES), 16, 1024);
+        const uint64_t dk = sdesc_sw128(smem_u32(sK + (c & 1) * TC::TILE_BYTES), 16, 1024);
+        if (elect_one()) {
+#pragma unroll
+          for (int kk = 0; kk < D / 16; ++kk) {
+            const uint32_t oa = ((kk >> 2) * (TBM * 128) + (kk & 3) * 32) >> 4;
+            mma_ss(tmem + t * 128, dq + oa, dk + oa, IDESC_QK, kk > 0);
+          }
+          mma_commit(&s_bar[t]);
+        }
+        __syncwarp();
+      };
+      for (int c = 0; c < chunks; ++c) {
+        mbar_wait(&kv_full[c & 1], (c >> 1) & 1);
+        tc_fence_after();
+#pragma unroll
+        for (int t = 0; t < NS; ++t) {
+          if (c > 0) pv(t, c - 1);
+          qk(t, c);
         }
       }
-      cp_async_wait_all();
-      fence_proxy_async();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&kv_full[b]);
-    }
-  } else if (warp == 4) {
-    // ------------------------------------------------------------ tcgen05 issue
-    if (lane == 0) {
-      mbar_arrive_expect_tx(&q_full, TC::TILE_BYTES);
+      if (chunks > 0)
 #pragma unroll
-      for (int b = 0; b < TC::NBOX; ++b)
-        tma_load_3d(sQ + b * (TBM * 128), &tmap_q, &q_full, b * 64, row0, bh);
+        for (int t = 0; t < NS; ++t) pv(t, chunks - 1);
     }
-    constexpr uint32_t IDESC_QK = idesc_bf16_f32(TBM, TBM, 0, 0);
-    constexpr uint32_t IDESC_PV = idesc_bf16_f32(TBM, D, 0, 1);
-    const uint64_t dq = sdesc_sw128(smem_u32(sQ), 16, 1024);
-    mbar_wait(&q_full, 0);
-    auto pv = [&](int c) {                                  // O += P_c V_c
-      mbar_wait(&p_bar, c & 1);
-      tc_fence_after();
-      const int b = c & 1;
-      const uint64_t dv = sdesc_sw128(smem_u32(sV + b * TC::TILE_BYTES), TBM * 128, 1024);
-      if (elect_one()) {
-#pragma unroll
-        for (int kk = 0; kk < TBM / 16; ++kk)
-          mma_ts(tmem + 128, tmem + kk * 8, dv + ((uint32_t)(kk * 2048) >> 4), IDESC_PV,
-                 (c > 0 || kk > 0) ? 1u : 0u);
-        mma_commit(&kv_empty[b]);
-        mma_commit(&pv_done);
-      }
-      __syncwarp();
-    };
-    for (int c = 0; c < chunks; ++c) {
-      const int b = c & 1;
-      mbar_wait(&kv_full[b], (c >> 1) & 1);
-      if (c > 0) pv(c - 1);
-      tc_fence_after();
-      const uint64_t dk = sdesc_sw128(smem_u32(sK + b * TC::TILE_BYTES), 16, 1024);
-      if (elect_one()) {
-#pragma unroll
-        for (int kk = 0; kk < D / 16; ++kk) {
-          const uint32_t oa = ((kk >> 2) * (TBM * 128) + (kk & 3) * 32) >> 4;
-          mma_ss(tmem, dq + oa, dk + oa, IDESC_QK, kk > 0);
-        }
-        mma_commit(&s_bar);
-      }
-      __syncwarp();
-    }
-    if (chunks > 0) pv(chunks - 1);
-  } else {
+  } else if (warp < 4 * NS) {
     // ------------------------------------------------------------ softmax, one row per thread
-    const int row = warp * 32 + lane;
-    const uint32_t t_row = tmem + (uint32_t(warp * 32) << 16);
+    reg_alloc<TOK_REG_SOFTMAX>();
+    const int t = warp >> 2;
+    const int row = (warp & 3) * 32 + lane;
+    const uint32_t t_row = tmem + (uint32_t((warp & 3) * 32) << 16);
+    const uint32_t s_col = t * 128, o_col = 256 + t * 128;
     float m = -INFINITY, l = 0.f;
     for (int c = 0; c < chunks; ++c) {
-      mbar_wait(&s_bar, c & 1);
+      mbar_wait(&s_bar[t], c & 1);
       tc_fence_after();
       uint32_t s[TBM];
 #pragma unroll
-      for (int c0 = 0; c0 < TBM; c0 += 32) tmem_ld32(t_row + c0, s + c0);
+      for (int c0 = 0; c0 < TBM; c0 += 32) tmem_ld32(t_row + s_col + c0, s + c0);
       tmem_wait_ld();
       const int valid = min(TBM, n - c * TBM);
       if (valid < TBM) {
@@ -280,21 +301,23 @@ __global__ void __launch_bounds__(TOK_THREADS, 1) token_attn_kernel(
 #pragma unroll
       for (int i = 0; i < TBM; i += 2) mx = fmax3(mx, __uint_as_float(s[i]), __uint_as_float(s[i + 1]));
       const float mx_s = mx * scale_log2;
-      if (mx_s > m + 8.0f) {
-        // S_c complete => P_{c-1} V_{c-1} complete (issued before it, in order)
-        const float alpha = ex2(m - mx_s);
+      const bool need = mx_s > m + 8.0f;
+      float alpha = 1.f;
+      if (need) {
+        alpha = ex2(m - mx_s);
         l *= alpha;
         m = mx_s;
-        if (c > 0) {
+      }
+      // S_t,c complete => P_t,c-1 V_c-1 complete (issued before it): O may be rescaled now
+      if (c > 0 && __any_sync(0xffffffffu, need)) {
 #pragma unroll 1
-          for (int c0 = 0; c0 < D; c0 += 32) {
-            uint32_t ov[32];
-            tmem_ld32(t_row + 128 + c0, ov);
-            tmem_wait_ld();
+        for (int c0 = 0; c0 < D; c0 += 32) {
+          uint32_t ov[32];
+          tmem_ld32(t_row + o_col + c0, ov);
+          tmem_wait_ld();
 #pragma unroll
-            for (int i = 0; i < 32; ++i) ov[i] = __float_as_uint(__uint_as_float(ov[i]) * alpha);
-            tmem_st32(t_row + 128 + c0, ov);
-          }
+          for (int i = 0; i < 32; ++i) ov[i] = __float_as_uint(__uint_as_float(ov[i]) * alpha);
+          tmem_st32(t_row + o_col + c0, ov);
         }
       }
       const float mref = (m == -INFINITY) ? 0.f : m;
@@ -309,25 +332,25 @@ __global__ void __launch_bounds__(TOK_THREADS, 1) token_attn_kernel(
           sum += p0 + p1;
           pk[i / 2] = pack_bf16x2(p0, p1);
         }
-        tmem_st16(t_row + c0 / 2, pk);
+        tmem_st16(t_row + s_col + c0 / 2, pk);
       }
       l += sum;
       tmem_wait_st();
       tc_fence_before();
-      mbar_arrive(&p_bar);
+      mbar_arrive(&p_bar[t]);
     }
     // epilogue: O / l -> bf16 rows of this query block
-    const int q = row0 + row;
-    const bool store = q < row_end && sub * TBM + row < C;
+    const int q = g * C + t * TBM + row;
+    const bool store = q < row_end && t * TBM + row < C;
     uint16_t* orow = o + (long long)bh * o_stride + (long long)q * D;
     if (chunks > 0) {
-      mbar_wait(&pv_done, (chunks - 1) & 1);
+      mbar_wait(&pv_done[t], (chunks - 1) & 1);
       tc_fence_after();
       const float inv = 1.f / l;
 #pragma unroll 1
       for (int c0 = 0; c0 < D; c0 += 16) {
         uint32_t ov[16];
-        tmem_ld16(t_row + 128 + c0, ov);
+        tmem_ld16(t_row + o_col + c0, ov);
         tmem_wait_ld();
         uint32_t pk[8];
 #pragma unroll
@@ -342,12 +365,17 @@ __global__ void __launch_bounds__(TOK_THREADS, 1) token_attn_kernel(
     } else if (store) {
       for (int c0 = 0; c0 < D; c0 += 8) *reinterpret_cast<uint4*>(orow + c0) = make_uint4(0, 0, 0, 0);
     }
+    reg_dealloc<128>();
+  } else {
+    // warps of an unused second slot (C <= 128)
+    reg_alloc<TOK_REG_SOFTMAX>();
+    reg_dealloc<128>();
   }
   tc_fence_before();
   __syncthreads();
-  if (warp == 4) {
+  if (warp == TOK_WARP_MMA) {
     tc_fence_after();
-    tmem_dealloc(tmem, 256);
+    tmem_dealloc(tmem, 512);
   }
 }
 
@@ -377,22 +405,22 @@ cudaError_t launch_token_attn(int head_dim, const CUtensorMap& tq, const uint16_
                               float scale_log2, const int* row_ptr, const int* col_idx,
                               uint16_t* o, long long o_stride, cudaStream_t st) {
   const int G = (n_q + C - 1) / C;
-  const int subs = (C + TBM - 1) / TBM;
-  const long long items = (long long)bh * G * subs;
+  const int ns = (C + TBM - 1) / TBM;
+  const long long items = (long long)bh * G;
   if (items <= 0) return cudaSuccess;
-  if (items > (1LL << 31) - 1) return cudaErrorInvalidValue;
-#define SV_TOK(D_)                                                                            \
-  if (head_dim == D_) {                                                                       \
-    auto kern = token_attn_kernel<D_>;                                                        \
+  if (items > (1LL << 31) - 1 || ns > 2) return cudaErrorInvalidValue;
+#define SV_TOK(D_, NS_)                                                                       \
+  if (head_dim == D_ && ns == NS_) {                                                          \
+    auto kern = token_attn_kernel<D_, NS_>;                                                   \
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,    \
                                          TokCfg<D_>::SMEM);                                   \
     if (e != cudaSuccess) return e;                                                           \
-    kern<<<(unsigned)items, TOK_THREADS, TokCfg<D_>::SMEM, st>>>(tq, k, v, kv_stride, n_q, C, G, subs, \
-                                                          scale_log2, row_ptr, col_idx, o,     \
-                                                          o_stride);                          \
+    kern<<<(unsigned)items, TOK_THREADS, TokCfg<D_>::SMEM, st>>>(tq, k, v, kv_stride, n_q, C, G, \
+                                                              scale_log2, row_ptr, col_idx, o, \
+                                                              o_stride);                      \
     return cudaGetLastError();                                                                \
   }
-  SV_TOK(128) SV_TOK(64)
+  SV_TOK(128, 1) SV_TOK(128, 2) SV_TOK(64, 1) SV_TOK(64, 2)
 #undef SV_TOK
   return cudaErrorInvalidValue;
 }
