@@ -2,9 +2,9 @@
 //
 //  * colsum_kernel: A^(S)[g, j] = sum_{q in query block g} P[q, j]
 //    over query blocks of C rows.  Computed transposed, S^T = K Q_g^T (tcgen05, M = 128 keys,
-//    N = C queries, accumulator in TMEM), so each thread owns one key row and the column sum of
-//    P is the row sum sum_q 2^(s_jq * scale * log2 e - L_q) with L_q = lse_q * log2 e taken from
-//    the decision scale's dense pass: no cross-thread reduction, fp32 throughout.
+//    N = C queries, double-buffered accumulators in TMEM), so each thread owns one key row and
+//    the column sum of P is the row sum sum_q 2^(s_jq * scale * log2 e - L_q) with
+//    L_q = lse_q * log2 e from the decision scale's dense pass: no cross-thread reduction, fp32.
 //  * token_attn_kernel: Delta O^(K) over per-query-block token lists (PAPER.md:318-328,
 //    824-830 "gathers discrete, non-contiguous key and value vectors ... packed into contiguous
 //    dense tiles within shared memory"): a producer warp gathers 128 listed K and V rows per
@@ -14,6 +14,7 @@
 //    (b,h, query block): the block's 128-row sub-tiles are two slots sharing every gathered
 //    chunk; seven gather warps fill double-buffered K/V chunks.
 #include <cuda_bf16.h>
+#include <algorithm>
 #include <cstdio>
 
 #include "kernels.h"
@@ -26,38 +27,51 @@ namespace {
 constexpr int TBM = 128;           // key rows per colsum tile / query rows per attention tile
 
 // ------------------------------------------------------------------------------- column sums
+// One CTA per (b,h, query block g, range of key tiles).  Warp 8 loads the block's Q once and
+// streams 128-key tiles of K through a 2-stage TMA ring; it issues S^T = K Q_g^T into one of two
+// TMEM accumulators (C columns each).  Warpgroup s (warps 4s..4s+3) exponentiates the tiles of
+// accumulator s (one key row per thread: sum_q 2^(s * scale * log2 e - L_q)), so two softmax
+// warps per SM sub-partition keep the MUFU pipe busy while the next MMA runs.
 template <int D, int C>
 struct ColCfg {
   static constexpr int NBOX = D / 64;
   static constexpr int K_BYTES = TBM * D * 2;
   static constexpr int Q_BYTES = C * D * 2;
-  static constexpr int SMEM = K_BYTES + Q_BYTES + C * 4 + 1024;   // + alignment slack
+  static constexpr int SMEM = 2 * K_BYTES + Q_BYTES + C * 4 + 1024;   // + alignment slack
 };
 
 template <int D, int C>
-__global__ void __launch_bounds__(128) colsum_kernel(const __grid_constant__ CUtensorMap tmap_k,
-                                                     const __grid_constant__ CUtensorMap tmap_q,
-                                                     int n_q, int n_kv, int G, float scale_log2,
-                                                     const float* __restrict__ lse,
-                                                     float* __restrict__ out) {
+__global__ void __launch_bounds__(288, 1) colsum_kernel(const __grid_constant__ CUtensorMap tmap_k,
+                                                        const __grid_constant__ CUtensorMap tmap_q,
+                                                        int n_q, int n_kv, int G, int n_kt,
+                                                        int tiles_per_cta, float scale_log2,
+                                                        const float* __restrict__ lse,
+                                                        float* __restrict__ out) {
   using CF = ColCfg<D, C>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~uintptr_t(1023));       // SW128 tiles: 1 KB aligned
-  uint8_t* sK = smem;
-  uint8_t* sQ = smem + CF::K_BYTES;
-  float* sL = reinterpret_cast<float*>(sQ + CF::Q_BYTES);
-  __shared__ uint64_t bar_load, bar_mma;
+  uint8_t* sQ = smem;
+  uint8_t* sK = smem + CF::Q_BYTES;                          // [2]
+  float* sL = reinterpret_cast<float*>(sK + 2 * CF::K_BYTES);
+  __shared__ uint64_t q_full, k_full[2], k_free[2], acc_full[2], acc_free[2];
   __shared__ uint32_t tslot;
-  const int kt = blockIdx.x, g = blockIdx.y, bh = blockIdx.z;
+  const int kt0 = blockIdx.x * tiles_per_cta;
+  const int nt = min(tiles_per_cta, n_kt - kt0);
+  const int g = blockIdx.y, bh = blockIdx.z;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
-    mbar_init(&bar_load, 1);
-    mbar_init(&bar_mma, 1);
+    mbar_init(&q_full, 1);
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&k_full[b], 1);
+      mbar_init(&k_free[b], 1);
+      mbar_init(&acc_full[b], 1);
+      mbar_init(&acc_free[b], TBM);
+    }
     fence_barrier_init();
   }
-  if (warp == 0) {
-    tmem_alloc(&tslot, 256);
+  if (warp == 8) {
+    tmem_alloc(&tslot, 512);
     tmem_relinquish();
   }
   // L_q of the block's queries; rows past N_S contribute 2^-inf = 0
@@ -68,51 +82,83 @@ __global__ void __launch_bounds__(128) colsum_kernel(const __grid_constant__ CUt
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  const uint32_t tmem = tslot;
-  if (threadIdx.x == 0) {
-    mbar_arrive_expect_tx(&bar_load, CF::K_BYTES + CF::Q_BYTES);
+  const uint32_t tmem = tslot;                              // accumulator b: cols [256 b, +C)
+  if (warp == 8) {
+    if (lane == 0) {
+      mbar_arrive_expect_tx(&q_full, CF::Q_BYTES);
 #pragma unroll
-    for (int b = 0; b < CF::NBOX; ++b) {
-      tma_load_3d(sK + b * (TBM * 128), &tmap_k, &bar_load, b * 64, kt * TBM, bh);
-      tma_load_3d(sQ + b * (C * 128), &tmap_q, &bar_load, b * 64, g * C, bh);
-    }
-  }
-  if (warp == 0) {
-    mbar_wait(&bar_load, 0);
-    tc_fence_after();
-    if (elect_one()) {
-      constexpr uint32_t IDESC = idesc_bf16_f32(TBM, C, 0, 0);
-      const uint64_t da = sdesc_sw128(smem_u32(sK), 16, 1024);
-      const uint64_t db = sdesc_sw128(smem_u32(sQ), 16, 1024);
+      for (int b = 0; b < CF::NBOX; ++b)
+        tma_load_3d(sQ + b * (C * 128), &tmap_q, &q_full, b * 64, g * C, bh);
+      // K ring: the load of tile i+2 waits for the MMA of tile i to have read its stage
+      for (int i = 0; i < min(nt, 2); ++i) {
+        mbar_arrive_expect_tx(&k_full[i], CF::K_BYTES);
 #pragma unroll
-      for (int kk = 0; kk < D / 16; ++kk) {
-        const uint32_t oa = ((kk >> 2) * (TBM * 128) + (kk & 3) * 32) >> 4;
-        const uint32_t ob = ((kk >> 2) * (C * 128) + (kk & 3) * 32) >> 4;
-        mma_ss(tmem, da + oa, db + ob, IDESC, kk > 0);
+        for (int b = 0; b < CF::NBOX; ++b)
+          tma_load_3d(sK + i * CF::K_BYTES + b * (TBM * 128), &tmap_k, &k_full[i], b * 64,
+                      (kt0 + i) * TBM, bh);
       }
-      mma_commit(&bar_mma);
     }
     __syncwarp();
-  }
-  mbar_wait(&bar_mma, 0);
-  tc_fence_after();
-  const uint32_t t_row = tmem + (uint32_t(warp * 32) << 16);
-  float acc = 0.f;
-#pragma unroll 1
-  for (int c0 = 0; c0 < C; c0 += 32) {
-    uint32_t s[32];
-    tmem_ld32(t_row + c0, s);
-    tmem_wait_ld();
+    constexpr uint32_t IDESC = idesc_bf16_f32(TBM, C, 0, 0);
+    const uint64_t db = sdesc_sw128(smem_u32(sQ), 16, 1024);
+    mbar_wait(&q_full, 0);
+    for (int i = 0; i < nt; ++i) {
+      const int s = i & 1;
+      mbar_wait(&k_full[s], (i >> 1) & 1);
+      if (i >= 2) mbar_wait(&acc_free[s], ((i >> 1) - 1) & 1);
+      tc_fence_after();
+      const uint64_t da = sdesc_sw128(smem_u32(sK + s * CF::K_BYTES), 16, 1024);
+      if (elect_one()) {
 #pragma unroll
-    for (int i = 0; i < 32; ++i) acc += ex2(__uint_as_float(s[i]) * scale_log2 - sL[c0 + i]);
+        for (int kk = 0; kk < D / 16; ++kk) {
+          const uint32_t oa = ((kk >> 2) * (TBM * 128) + (kk & 3) * 32) >> 4;
+          const uint32_t ob = ((kk >> 2) * (C * 128) + (kk & 3) * 32) >> 4;
+          mma_ss(tmem + s * 256, da + oa, db + ob, IDESC, kk > 0);
+        }
+        mma_commit(&acc_full[s]);
+        mma_commit(&k_free[s]);
+      }
+      __syncwarp();
+      if (i + 2 < nt && lane == 0) {
+        mbar_wait(&k_free[s], (i >> 1) & 1);
+        mbar_arrive_expect_tx(&k_full[s], CF::K_BYTES);
+#pragma unroll
+        for (int b = 0; b < CF::NBOX; ++b)
+          tma_load_3d(sK + s * CF::K_BYTES + b * (TBM * 128), &tmap_k, &k_full[s], b * 64,
+                      (kt0 + i + 2) * TBM, bh);
+      }
+      __syncwarp();
+    }
+  } else {
+    // warpgroup s exponentiates the tiles of accumulator s (tiles i with i % 2 == s)
+    const int s = warp >> 2;
+    const uint32_t t_row = tmem + (uint32_t((warp & 3) * 32) << 16);
+    for (int i = s; i < nt; i += 2) {
+      mbar_wait(&acc_full[s], (i >> 1) & 1);
+      tc_fence_after();
+      float acc0 = 0.f, acc1 = 0.f;
+#pragma unroll
+      for (int c0 = 0; c0 < C; c0 += 32) {
+        uint32_t v[32];
+        tmem_ld32(t_row + s * 256 + c0, v);
+        tmem_wait_ld();
+#pragma unroll
+        for (int t = 0; t < 32; t += 2) {
+          acc0 += ex2(__uint_as_float(v[t]) * scale_log2 - sL[c0 + t]);
+          acc1 += ex2(__uint_as_float(v[t + 1]) * scale_log2 - sL[c0 + t + 1]);
+        }
+      }
+      tc_fence_before();
+      mbar_arrive(&acc_free[s]);
+      const int j = (kt0 + i) * TBM + (warp & 3) * 32 + lane;
+      if (j < n_kv) out[((long long)bh * G + g) * n_kv + j] = acc0 + acc1;
+    }
   }
-  const int j = kt * TBM + warp * 32 + lane;
-  if (j < n_kv) out[((long long)bh * G + g) * n_kv + j] = acc;
   tc_fence_before();
   __syncthreads();
-  if (warp == 0) {
+  if (warp == 8) {
     tc_fence_after();
-    tmem_dealloc(tmem, 256);
+    tmem_dealloc(tmem, 512);
   }
 }
 
@@ -385,14 +431,20 @@ cudaError_t launch_colsum(int head_dim, int C, const CUtensorMap& tk, const CUte
                           int bh, int n_q, int n_kv, float scale_log2, const float* lse,
                           float* out, cudaStream_t st) {
   const int G = (n_q + C - 1) / C;
-  const dim3 grid((n_kv + TBM - 1) / TBM, G, bh);
+  const int n_kt = (n_kv + TBM - 1) / TBM;
+  // whole rows of key tiles per CTA (the Q load and pipeline fill amortised over the row) unless
+  // there are too few (b,h,g) rows to give every SM two CTAs' worth of work
+  const long long rows = (long long)G * bh;
+  const int splits = (int)std::min<long long>(n_kt, std::max<long long>(1, (2LL * 148 + rows - 1) / rows));
+  const int tpc = (n_kt + splits - 1) / splits;
+  const dim3 grid((n_kt + tpc - 1) / tpc, G, bh);
 #define SV_COL(D_, C_)                                                                       \
   if (head_dim == D_ && C == C_) {                                                           \
     auto kern = colsum_kernel<D_, C_>;                                                       \
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,   \
                                          ColCfg<D_, C_>::SMEM);                              \
     if (e != cudaSuccess) return e;                                                          \
-    kern<<<grid, 128, ColCfg<D_, C_>::SMEM, st>>>(tk, tq, n_q, n_kv, G, scale_log2, lse, out); \
+    kern<<<grid, 288, ColCfg<D_, C_>::SMEM, st>>>(tk, tq, n_q, n_kv, G, n_kt, tpc, scale_log2, lse, out); \
     return cudaGetLastError();                                                               \
   }
   SV_COL(128, 192) SV_COL(128, 128) SV_COL(128, 64) SV_COL(64, 192) SV_COL(64, 128) SV_COL(64, 64)
