@@ -16,12 +16,17 @@ Definitions followed
   Delta O^(K) for the rows of block g_K: Softmax(q K_J^T / sqrt(d)) V_J over the tokens J(g_K)
         it selects
 
+  O_cache on the token path: O_cache^(S) = O_dense^(S) - Delta O^(S) over inds^(S), reused at K
+        through the nearest-neighbour upsampling of oracle/cache.py
+
 Pins (tests/test_oracle_token_cs4a.py): column sums of every block add up to its row count
 (softmax rows sum to 1) and equal a per-element exp-loop brute force on a tiny schedule; top-k
 with k >= C_S selects every key and picks a planted dominant key at k = 1; the token map at S = K
 is the identity plus the sink, and its block-OR equals the (separately pinned) block mapping of
 the block-OR of the source selection when C = B; token-sparse attention with every token equals
-dense attention and with the tokens of whole blocks equals the block-sparse oracle.
+dense attention and with the tokens of whole blocks equals the block-sparse oracle; the token
+O_cache vanishes when every token is selected and equals the (pinned) block O_cache when whole
+blocks are selected.
 """
 from __future__ import annotations
 
@@ -29,7 +34,8 @@ import math
 
 import numpy as np
 
-from .attention import softmax_rows
+from .attention import dense, softmax_rows
+from .cache import upsample_nn
 from .geometry import Schedule, ceil_div
 from .mapping import map_token, phi
 
@@ -87,3 +93,14 @@ def token_sparse(q: np.ndarray, k: np.ndarray, v: np.ndarray, C: int, sel: np.nd
         qg = q[g * C:min((g + 1) * C, n_q)]
         out[g * C:g * C + len(qg)] = softmax_rows((qg @ k[J].T) / math.sqrt(D)) @ v[J]
     return out
+
+
+def token_cache_residual(q_S, k, v, n_kv_S: int, C: int, sel_S: np.ndarray) -> np.ndarray:
+    """O_cache^(S) for one (b, h): dense minus token-sparse attention at S."""
+    return dense(q_S, k, v, n_kv_S) - token_sparse(q_S, k, v, C, sel_S)
+
+
+def token_cached_sparse(q_k, k, v, C: int, sel_k: np.ndarray, o_cache_S: np.ndarray, s_S: int,
+                        s_k: int) -> np.ndarray:
+    """O^(k) ~= upsample(O_cache^(S)) + Delta O^(k) on the token path."""
+    return token_sparse(q_k, k, v, C, sel_k) + upsample_nn(o_cache_S, s_S, s_k)

@@ -7,7 +7,9 @@ import pytest
 from oracle.attention import block_sparse, dense
 from oracle.geometry import Schedule, ceil_div
 from oracle.mapping import map_pattern
-from oracle.token_cs4a import colsum, map_tokens, select_tokens, token_sparse, topk_count
+from oracle.cache import cache_residual
+from oracle.token_cs4a import (colsum, map_tokens, select_tokens, token_cache_residual, token_sparse,
+                               topk_count)
 
 TINY = Schedule([1, 2, 4, 8])          # C = 1, 5, 21, 85
 EQ = Schedule([1, 2, 4, 6, 8, 12, 16])
@@ -96,3 +98,16 @@ def test_token_sparse_reduces_to_dense_and_block_sparse():
     sel = np.repeat(blk, C, axis=1)[:, :n_kv]
     want = block_sparse(q, k, v, n_kv, C, [np.nonzero(r)[0] for r in blk])
     assert np.allclose(token_sparse(q, k, v, C, sel), want, atol=1e-12)
+
+
+def test_token_cache_residual():
+    n_q, n_kv, D, C = EQ.N(5), EQ.C(5), 16, 16
+    q, k, v = _rand(10, n_q, D), _rand(11, n_kv, D), _rand(12, n_kv, D)
+    G = ceil_div(n_q, C)
+    assert np.abs(token_cache_residual(q, k, v, n_kv, C, np.ones((G, n_kv), bool))).max() < 1e-12
+    rng = np.random.default_rng(13)
+    blk = rng.random((G, ceil_div(n_kv, C))) < 0.4
+    blk[:, 0] = True
+    sel = np.repeat(blk, C, axis=1)[:, :n_kv]
+    want = cache_residual(q, k, v, n_kv, C, [np.nonzero(r)[0] for r in blk])
+    assert np.allclose(token_cache_residual(q, k, v, n_kv, C, sel), want, atol=1e-12)
