@@ -252,6 +252,27 @@ sparvar_status sparvar_token_sparse_attn(const sparvar_schedule* sched, int32_t 
                                          const uint16_t* v_cache, const int32_t* row_ptr,
                                          const int32_t* col_idx, float softmax_scale, uint16_t* o,
                                          void* stream);
+/* Token-level O_cache (PAPER.md:289-334 on the token path): sparvar_token_cache_residual runs
+ *   the token-list attention at the decision scale over its own selection (lists of
+ *   sparvar_token_select's rows) into o_cache and subtracts it from o_dense (the dense output at
+ *   S) in place: o_cache = o_dense - Softmax(Q K_inds^T) V_inds.  sparvar_token_sparse_attn_cached
+ *   is sparvar_token_sparse_attn with the nearest-neighbour upsampled o_cache (side of
+ *   cache_scale, cache_stride_bh elements per (b,h)) added in its epilogue (READING 22); empty
+ *   lists give the cache row.  Errors as for sparvar_cache_residual / _block_sparse_attn_cached.
+ */
+sparvar_status sparvar_token_cache_residual(const sparvar_schedule* sched, int32_t decision_scale,
+                                            int32_t query_block, const sparvar_attn_shape* shape,
+                                            const uint16_t* q_S, const uint16_t* k_cache,
+                                            const uint16_t* v_cache, const int32_t* row_ptr_S,
+                                            const int32_t* col_idx_S, float softmax_scale,
+                                            const uint16_t* o_dense, uint16_t* o_cache,
+                                            void* stream);
+sparvar_status sparvar_token_sparse_attn_cached(
+    const sparvar_schedule* sched, int32_t target_scale, int32_t query_block,
+    const sparvar_attn_shape* shape, const uint16_t* q, const uint16_t* k_cache,
+    const uint16_t* v_cache, const int32_t* row_ptr, const int32_t* col_idx, float softmax_scale,
+    const uint16_t* o_cache, int32_t cache_scale, int64_t cache_stride_bh, uint16_t* o,
+    void* stream);
 
 /* NEXT(1) — cached block-sparse attention at scale K:
  *   O^(K) = Upsample(O_cache) + Delta O^(K), Delta O^(K) = sparvar_block_sparse_attn output.

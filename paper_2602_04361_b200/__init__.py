@@ -24,6 +24,7 @@ __all__ = [
     "build_block_lists", "block_sparse_attn", "dense_attn", "cache_residual",
     "block_sparse_attn_cached", "cache_residual_from_dense", "dense_attn_mass",
     "dense_attn_mass_workspace", "token_colsum", "token_select", "token_map", "token_sparse_attn",
+    "token_cache_residual", "token_sparse_attn_cached",
     "SparseLayer", "unpack_bits",
     "SELECT_TOPK", "SELECT_THRESHOLD", "MAP_FOOTPRINT", "MAP_POINT",
 ]
@@ -79,6 +80,9 @@ def _load(path: str = LIB_PATH, partial: bool = False):
         "sparvar_token_select": [S, I32, I32, I32, I32, P, I32, P, P],
         "sparvar_token_map": [S, I32, I32, I32, I32, I32, I32, P, P, P],
         "sparvar_token_sparse_attn": [S, I32, I32, SH, P, P, P, P, P, F32, P, P],
+        "sparvar_token_cache_residual": [S, I32, I32, SH, P, P, P, P, P, F32, P, P, P],
+        "sparvar_token_sparse_attn_cached": [S, I32, I32, SH, P, P, P, P, P, F32, P, I32, I64, P,
+                                             P],
     }
     for name, args in sig.items():
         if partial and not hasattr(L, name):
@@ -358,6 +362,37 @@ def token_sparse_attn(sides, target: int, C: int, q, k_cache, v_cache, row_ptr, 
     _check(lib.sparvar_token_sparse_attn(ctypes.byref(_sched(sides)), target, C, ctypes.byref(sh),
                                          _ptr(q), _ptr(k_cache), _ptr(v_cache), _ptr(row_ptr),
                                          _ptr(col_idx), softmax_scale, _ptr(o), _stream(stream)))
+    return o
+
+
+def token_cache_residual(sides, decision_scale: int, C: int, q_S, k_cache, v_cache, row_ptr_S,
+                         col_idx_S, o_dense, softmax_scale: float = 0.0, o_cache=None,
+                         stream=None):
+    """Token-level O_cache = o_dense - token attention at S over the selected tokens."""
+    if o_cache is None:
+        o_cache = torch.empty_like(q_S)
+    if _bh_view(o_dense, "o_dense") != o_cache.stride(0):
+        raise ValueError("o_dense and o_cache must share a (b,h) stride")
+    sh = _attn_shape(q_S, k_cache, o_cache)
+    _check(lib.sparvar_token_cache_residual(
+        ctypes.byref(_sched(sides)), decision_scale, C, ctypes.byref(sh), _ptr(q_S), _ptr(k_cache),
+        _ptr(v_cache), _ptr(row_ptr_S), _ptr(col_idx_S), softmax_scale, _ptr(o_dense),
+        _ptr(o_cache), _stream(stream)))
+    return o_cache
+
+
+def token_sparse_attn_cached(sides, target: int, C: int, q, k_cache, v_cache, row_ptr, col_idx,
+                             o_cache, cache_scale: int, softmax_scale: float = 0.0, o=None,
+                             stream=None):
+    """Token-list attention at K plus the NN-upsampled token-level O_cache."""
+    if o is None:
+        o = torch.empty_like(q)
+    cstride = _bh_view(o_cache, "o_cache")
+    sh = _attn_shape(q, k_cache, o)
+    _check(lib.sparvar_token_sparse_attn_cached(
+        ctypes.byref(_sched(sides)), target, C, ctypes.byref(sh), _ptr(q), _ptr(k_cache),
+        _ptr(v_cache), _ptr(row_ptr), _ptr(col_idx), softmax_scale, _ptr(o_cache), cache_scale,
+        cstride, _ptr(o), _stream(stream)))
     return o
 
 

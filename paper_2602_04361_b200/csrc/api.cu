@@ -122,7 +122,7 @@ extern "C" {
 
 const char* sparvar_last_error(void) { return g_err.c_str(); }
 
-int32_t sparvar_version(void) { return 103; }   // 1.03: + token-level CS4A (NEXT(2))
+int32_t sparvar_version(void) { return 104; }   // 1.04: + token-level CS4A with O_cache (NEXT(2))
 
 sparvar_status sparvar_local_mask(const sparvar_schedule* sched, int32_t target_scale,
                                   int32_t block, int32_t sink_scales, const int32_t* windows,
@@ -457,12 +457,13 @@ sparvar_status sparvar_token_map(const sparvar_schedule* sched, int32_t src_scal
   return ok();
 }
 
-sparvar_status sparvar_token_sparse_attn(const sparvar_schedule* sched, int32_t target_scale,
-                                         int32_t query_block, const sparvar_attn_shape* shape,
-                                         const uint16_t* q, const uint16_t* k_cache,
-                                         const uint16_t* v_cache, const int32_t* row_ptr,
-                                         const int32_t* col_idx, float softmax_scale, uint16_t* o,
-                                         void* stream) {
+static sparvar_status token_attn_common(const sparvar_schedule* sched, int32_t target_scale,
+                                        int32_t query_block, const sparvar_attn_shape* shape,
+                                        const uint16_t* q, const uint16_t* k_cache,
+                                        const uint16_t* v_cache, const int32_t* row_ptr,
+                                        const int32_t* col_idx, float softmax_scale, uint16_t* o,
+                                        void* stream, const uint16_t* add = nullptr,
+                                        int32_t add_scale = 0, int64_t add_stride = 0) {
   sv::Geo g;
   sparvar_status s = make_geo(sched, &g);
   if (s != SPARVAR_OK) return s;
@@ -486,9 +487,62 @@ sparvar_status sparvar_token_sparse_attn(const sparvar_schedule* sched, int32_t 
   cudaError_t e = sv::launch_token_attn(D, tq, k_cache, v_cache, shape->kv_stride_bh,
                                         shape->batch_heads, (int)n_q, query_block,
                                         scale * 1.4426950408889634f, row_ptr, col_idx, o,
-                                        shape->o_stride_bh, (cudaStream_t)stream);
+                                        shape->o_stride_bh, add, add_stride,
+                                        add != nullptr ? g.side[add_scale - 1] : 1, g.side[K - 1],
+                                        (cudaStream_t)stream);
   if (e != cudaSuccess) return cuda_fail(e, "token attention launch");
   return ok();
+}
+
+sparvar_status sparvar_token_sparse_attn(const sparvar_schedule* sched, int32_t target_scale,
+                                         int32_t query_block, const sparvar_attn_shape* shape,
+                                         const uint16_t* q, const uint16_t* k_cache,
+                                         const uint16_t* v_cache, const int32_t* row_ptr,
+                                         const int32_t* col_idx, float softmax_scale, uint16_t* o,
+                                         void* stream) {
+  return token_attn_common(sched, target_scale, query_block, shape, q, k_cache, v_cache, row_ptr,
+                           col_idx, softmax_scale, o, stream);
+}
+
+sparvar_status sparvar_token_cache_residual(const sparvar_schedule* sched, int32_t decision_scale,
+                                            int32_t query_block, const sparvar_attn_shape* shape,
+                                            const uint16_t* q_S, const uint16_t* k_cache,
+                                            const uint16_t* v_cache, const int32_t* row_ptr_S,
+                                            const int32_t* col_idx_S, float softmax_scale,
+                                            const uint16_t* o_dense, uint16_t* o_cache,
+                                            void* stream) {
+  if (o_dense == nullptr || o_cache == nullptr)
+    return fail(SPARVAR_ERR_INVALID_ARG, "null o_dense / o_cache");
+  if (o_dense == o_cache) return fail(SPARVAR_ERR_INVALID_ARG, "o_cache must not alias o_dense");
+  if (!aligned16(o_dense)) return fail(SPARVAR_ERR_INVALID_ARG, "o_dense must be 16-byte aligned");
+  sparvar_status s = token_attn_common(sched, decision_scale, query_block, shape, q_S, k_cache,
+                                       v_cache, row_ptr_S, col_idx_S, softmax_scale, o_cache, stream);
+  if (s != SPARVAR_OK) return s;
+  const int side = sched->sides[decision_scale - 1];
+  cudaError_t e = sv::launch_residual(shape->batch_heads, side * side, shape->head_dim, o_dense,
+                                      shape->o_stride_bh, o_cache, shape->o_stride_bh, o_cache,
+                                      shape->o_stride_bh, (cudaStream_t)stream);
+  if (e != cudaSuccess) return cuda_fail(e, "residual launch");
+  return ok();
+}
+
+sparvar_status sparvar_token_sparse_attn_cached(
+    const sparvar_schedule* sched, int32_t target_scale, int32_t query_block,
+    const sparvar_attn_shape* shape, const uint16_t* q, const uint16_t* k_cache,
+    const uint16_t* v_cache, const int32_t* row_ptr, const int32_t* col_idx, float softmax_scale,
+    const uint16_t* o_cache, int32_t cache_scale, int64_t cache_stride_bh, uint16_t* o,
+    void* stream) {
+  if (o_cache == nullptr) return fail(SPARVAR_ERR_INVALID_ARG, "null o_cache");
+  if (sched == nullptr || cache_scale < 1 || cache_scale > target_scale ||
+      cache_scale > sched->num_scales)
+    return fail(SPARVAR_ERR_INVALID_ARG, "cache_scale %d not in [1, target_scale]", cache_scale);
+  if (shape == nullptr) return fail(SPARVAR_ERR_INVALID_ARG, "null shape");
+  const long long n_S = (long long)sched->sides[cache_scale - 1] * sched->sides[cache_scale - 1];
+  if (cache_stride_bh < n_S * shape->head_dim || cache_stride_bh % 8 != 0 || !aligned16(o_cache))
+    return fail(SPARVAR_ERR_INVALID_ARG, "cache_stride_bh must be >= N_S*D, a multiple of 8, "
+                "and o_cache 16-byte aligned");
+  return token_attn_common(sched, target_scale, query_block, shape, q, k_cache, v_cache, row_ptr,
+                           col_idx, softmax_scale, o, stream, o_cache, cache_scale, cache_stride_bh);
 }
 
 size_t sparvar_dense_attn_mass_workspace(const sparvar_schedule* sched, int32_t decision_scale,

@@ -76,7 +76,8 @@ cudaError_t launch_colsum(int head_dim, int C, const CUtensorMap& tk, const CUte
 cudaError_t launch_token_attn(int head_dim, const CUtensorMap& tq, const uint16_t* k,
                               const uint16_t* v, long long kv_stride, int bh, int n_q, int C,
                               float scale_log2, const int* row_ptr, const int* col_idx,
-                              uint16_t* o, long long o_stride, cudaStream_t st);
+                              uint16_t* o, long long o_stride, const uint16_t* add,
+                              long long add_stride, int s_src, int s_dst, cudaStream_t st);
 
 // ------------------------------------------------------------------ predictor.cu
 struct PredArgs {

@@ -189,6 +189,15 @@ __device__ __forceinline__ void fence_proxy_async() {
 // slot t: O_t += P_t,c-1 V_c-1, then S_t = Q_t K_c^T (S/P alias in TMEM and the tensor pipe runs
 // one thread's ops in order, so S_t,c complete also means P_t,c-1 V_c-1 is, which the softmax
 // needs before an O rescale).  The two slots' softmax chains interleave on the tensor pipe.
+// Optional NEXT(1) residual for the token path: out += NN-upsample(add) over the query grid
+// (READING 22): output query (x, y) of side s_dst adds cache row
+// (floor(x s_src / s_dst), floor(y s_src / s_dst)) of side s_src.
+struct TokCache {
+  const uint16_t* add;   // bf16 [bh][s_src * s_src][D] or nullptr
+  long long add_stride;  // elements between (b,h) slabs
+  int s_src, s_dst;
+};
+
 constexpr int TOK_WARPS = 16;
 constexpr int TOK_THREADS = TOK_WARPS * 32;
 constexpr int TOK_WARP_MMA = 8, TOK_WARP_GATHER0 = 9;
@@ -201,7 +210,7 @@ __global__ void __launch_bounds__(TOK_THREADS, 1) token_attn_kernel(
     const __grid_constant__ CUtensorMap tmap_q, const uint16_t* __restrict__ k,
     const uint16_t* __restrict__ v, long long kv_stride, int n_q, int C, int G,
     float scale_log2, const int* __restrict__ row_ptr, const int* __restrict__ col_idx,
-    uint16_t* __restrict__ o, long long o_stride) {
+    uint16_t* __restrict__ o, long long o_stride, const TokCache cache) {
   using TC = TokCfg<D>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
@@ -389,6 +398,12 @@ __global__ void __launch_bounds__(TOK_THREADS, 1) token_attn_kernel(
     const int q = g * C + t * TBM + row;
     const bool store = q < row_end && t * TBM + row < C;
     uint16_t* orow = o + (long long)bh * o_stride + (long long)q * D;
+    const uint16_t* arow = nullptr;
+    if (cache.add != nullptr && store) {
+      const int x = q / cache.s_dst, y = q % cache.s_dst;
+      const int src = (x * cache.s_src / cache.s_dst) * cache.s_src + (y * cache.s_src / cache.s_dst);
+      arow = cache.add + (long long)bh * cache.add_stride + (long long)src * D;
+    }
     if (chunks > 0) {
       mbar_wait(&pv_done[t], (chunks - 1) & 1);
       tc_fence_after();
@@ -398,10 +413,25 @@ __global__ void __launch_bounds__(TOK_THREADS, 1) token_attn_kernel(
         uint32_t ov[16];
         tmem_ld16(t_row + o_col + c0, ov);
         tmem_wait_ld();
+        float ad[16];
+        if (arow != nullptr) {
+          const uint4 u0 = *reinterpret_cast<const uint4*>(arow + c0);
+          const uint4 u1 = *reinterpret_cast<const uint4*>(arow + c0 + 8);
+          const uint32_t w[8] = {u0.x, u0.y, u0.z, u0.w, u1.x, u1.y, u1.z, u1.w};
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            ad[2 * i] = __uint_as_float(w[i] << 16);
+            ad[2 * i + 1] = __uint_as_float(w[i] & 0xffff0000u);
+          }
+        } else {
+#pragma unroll
+          for (int i = 0; i < 16; ++i) ad[i] = 0.f;
+        }
         uint32_t pk[8];
 #pragma unroll
         for (int i = 0; i < 8; ++i)
-          pk[i] = pack_bf16x2(__uint_as_float(ov[2 * i]) * inv, __uint_as_float(ov[2 * i + 1]) * inv);
+          pk[i] = pack_bf16x2(fmaf(__uint_as_float(ov[2 * i]), inv, ad[2 * i]),
+                              fmaf(__uint_as_float(ov[2 * i + 1]), inv, ad[2 * i + 1]));
         if (store) {
           uint4* dst = reinterpret_cast<uint4*>(orow + c0);
           dst[0] = make_uint4(pk[0], pk[1], pk[2], pk[3]);
@@ -409,7 +439,10 @@ __global__ void __launch_bounds__(TOK_THREADS, 1) token_attn_kernel(
         }
       }
     } else if (store) {
-      for (int c0 = 0; c0 < D; c0 += 8) *reinterpret_cast<uint4*>(orow + c0) = make_uint4(0, 0, 0, 0);
+      // empty list: the output is the (upsampled) cache row, if any
+      for (int c0 = 0; c0 < D; c0 += 8)
+        *reinterpret_cast<uint4*>(orow + c0) =
+            arow != nullptr ? *reinterpret_cast<const uint4*>(arow + c0) : make_uint4(0, 0, 0, 0);
     }
     reg_dealloc<128>();
   } else {
@@ -455,9 +488,11 @@ cudaError_t launch_colsum(int head_dim, int C, const CUtensorMap& tk, const CUte
 cudaError_t launch_token_attn(int head_dim, const CUtensorMap& tq, const uint16_t* k,
                               const uint16_t* v, long long kv_stride, int bh, int n_q, int C,
                               float scale_log2, const int* row_ptr, const int* col_idx,
-                              uint16_t* o, long long o_stride, cudaStream_t st) {
+                              uint16_t* o, long long o_stride, const uint16_t* add,
+                              long long add_stride, int s_src, int s_dst, cudaStream_t st) {
   const int G = (n_q + C - 1) / C;
   const int ns = (C + TBM - 1) / TBM;
+  const TokCache cache{add, add_stride, s_src, s_dst};
   const long long items = (long long)bh * G;
   if (items <= 0) return cudaSuccess;
   if (items > (1LL << 31) - 1 || ns > 2) return cudaErrorInvalidValue;
@@ -469,7 +504,7 @@ cudaError_t launch_token_attn(int head_dim, const CUtensorMap& tq, const uint16_
     if (e != cudaSuccess) return e;                                                           \
     kern<<<(unsigned)items, TOK_THREADS, TokCfg<D_>::SMEM, st>>>(tq, k, v, kv_stride, n_q, C, G, \
                                                               scale_log2, row_ptr, col_idx, o, \
-                                                              o_stride);                      \
+                                                              o_stride, cache);               \
     return cudaGetLastError();                                                                \
   }
   SV_TOK(128, 1) SV_TOK(128, 2) SV_TOK(64, 1) SV_TOK(64, 2)

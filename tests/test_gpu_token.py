@@ -101,3 +101,29 @@ def test_all_tokens_is_dense(sv):
     for b in range(bh):
         mx, mean = attn_errors(to_np(o[b]), dense(to_np(q[b]), to_np(k[b]), to_np(v[b]), sched.C(S)))
         assert mx <= MAX_ABS and mean <= MEAN_ABS, (mx, mean)
+
+
+@pytest.mark.parametrize("sides,S,K,C,D,bh,sink,alpha", [CASES[0], CASES[2]], ids=[IDS[0], IDS[2]])
+def test_token_cache_path(sv, sides, S, K, C, D, bh, sink, alpha):
+    """Token-level O_cache at S and its upsampled reuse at K against the oracle."""
+    from oracle.token_cs4a import token_cache_residual, token_cached_sparse
+    sched, qS, qK, k, v, cs, sel, dst, o, k_tok = _run(sv, sides, S, K, C, D, bh, sink, alpha)
+    G_S, G_K = ceil_div(sched.N(S), C), ceil_div(sched.N(K), C)
+    o_dense = sv.dense_attn(sides, S, qS, k, v)
+    rpS, ciS, stS = sv.build_block_lists(bh, G_S, sched.C(S), [(sel, False)])
+    oc = sv.token_cache_residual(sides, S, C, qS, k, v, rpS, ciS, o_dense)
+    rpK, ciK, stK = sv.build_block_lists(bh, G_K, sched.C(K), [(dst, False)])
+    o2 = sv.token_sparse_attn_cached(sides, K, C, qK, k, v, rpK, ciK, oc, S)
+    torch.cuda.synchronize()
+    assert stS.item() == 0 and stK.item() == 0
+    got_sel = bits_to_bool(sel.cpu().numpy(), sched.C(S))
+    got_dst = bits_to_bool(dst.cpu().numpy(), sched.C(K))
+    for b in range(bh):
+        qb, kb, vb = to_np(qS[b]), to_np(k[b]), to_np(v[b])
+        want_oc = token_cache_residual(qb, kb, vb, sched.C(S), C, got_sel[b])
+        mx, mean = attn_errors(to_np(oc[b]), want_oc)
+        assert mx <= MAX_ABS and mean <= MEAN_ABS, ("o_cache", b, mx, mean)
+        want = token_cached_sparse(to_np(qK[b]), kb, vb, C, got_dst[b], want_oc, sides[S - 1],
+                                   sides[K - 1])
+        mx, mean = attn_errors(to_np(o2[b]), want)
+        assert mx <= MAX_ABS and mean <= MEAN_ABS, ("O^(K)", b, mx, mean)
