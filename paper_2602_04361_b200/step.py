@@ -12,6 +12,10 @@ scales S+1..K run block-sparse attention:
       for k in S+1..K:
           lists_k = CSR(map S->k of the pattern)                 (sparvar_map_indices, _build_block_lists)
           O_k     = NN-upsample(O_cache) + Delta O_k             (sparvar_block_sparse_attn_cached)
+  granularity="token" replaces the CS4A layers' block pattern by the paper's token-granular one
+  (NEXT(2)): dense attention at S with its LSE, column sums over
+  C-row query blocks, top-k tokens (alpha C_S) + sinks, token-level O_cache, and per target
+  scale the token map, its lists and the cached token-list attention.
   CSLA layers (the rest):
       O_S     = dense attention at S
       for k in S+1..K:  O_k = block-sparse attention over the CSLA local mask of k
@@ -27,9 +31,13 @@ from typing import Dict, List, Sequence
 
 import torch
 
+import math
+
 from . import (MAP_FOOTPRINT, SELECT_TOPK, block_sparse_attn, block_sparse_attn_cached,
                build_block_lists, cache_residual_from_dense, dense_attn, dense_attn_mass,
-               dense_attn_mass_workspace, geometry, local_mask, map_indices, predict_pattern)
+               dense_attn_mass_workspace, geometry, local_mask, map_indices, predict_pattern,
+               token_cache_residual, token_colsum, token_map, token_select,
+               token_sparse_attn_cached)
 
 
 def layer_split(layers: int, cs4a_fraction: float = 0.6) -> int:
@@ -48,7 +56,8 @@ class SparsifiedStep:
                  layers: int, head_dim: int = 128, cs4a_fraction: float = 0.6,
                  sink_scales: int = 5, windows=(7, 5, 3, 1, 1), select_mode=SELECT_TOPK,
                  topk: int = 5, threshold: float = 0.01, map_mode=MAP_FOOTPRINT,
-                 fused: bool = True):
+                 fused: bool = True, granularity: str = "block", query_block: int = 192,
+                 alpha: float = 0.2):
         if not 1 <= decision < target <= len(sides):
             raise ValueError("need 1 <= decision < target <= number of scales")
         self.sides, self.S, self.K, self.B, self.bh = list(sides), decision, target, block, bh
@@ -74,11 +83,54 @@ class SparsifiedStep:
         self.fused = fused
         self.ws = torch.empty(max(1, dense_attn_mass_workspace(sides, decision, block, bh)) if fused
                               else 1, dtype=torch.uint8, device=dev)
+        if granularity not in ("block", "token"):
+            raise ValueError("granularity is 'block' or 'token'")
+        self.granularity, self.C = granularity, query_block
+        if granularity == "token":
+            C, n_S, c_S = query_block, sides[decision - 1] ** 2, sum(x * x for x in sides[:decision])
+            self.k_tok = max(1, math.ceil(alpha * c_S))                    # READING 11
+            self.tG_S = -(-n_S // C)
+            self.lse = torch.empty((bh, n_S), dtype=torch.float32, device=dev)
+            self.colsum = torch.empty((bh, self.tG_S, c_S), dtype=torch.float32, device=dev)
+            self.tsel = torch.empty((bh, self.tG_S, -(-c_S // 32)), dtype=torch.int32, device=dev)
+            self.tlists_S = self._tlists(self.tG_S, c_S)
+            self.tG, self.tmap, self.tlists = {}, {}, {}
+            for k in self.targets:
+                n_k, c_k = sides[k - 1] ** 2, sum(x * x for x in sides[:k])
+                self.tG[k] = -(-n_k // C)
+                self.tmap[k] = torch.empty((bh, self.tG[k], -(-c_k // 32)), dtype=torch.int32,
+                                           device=dev)
+                self.tlists[k] = self._tlists(self.tG[k], c_k)
 
     def _lists(self, g):
         cap = self.bh * g["G_q"] * g["G_kv"]
         return (torch.empty(self.bh * g["G_q"] + 1, dtype=torch.int32, device="cuda"),
                 torch.empty(cap, dtype=torch.int32, device="cuda"), cap)
+
+    def _tlists(self, G, n_tokens):
+        cap = self.bh * G * n_tokens
+        return (torch.empty(self.bh * G + 1, dtype=torch.int32, device="cuda"),
+                torch.empty(cap, dtype=torch.int32, device="cuda"), cap, G, n_tokens)
+
+    def _token_cs4a(self, q, k_cache, v_cache, out, stream):
+        S, C = self.S, self.C
+        dense_attn(self.sides, S, q[S], k_cache, v_cache, o=out[S], lse=self.lse, stream=stream)
+        token_colsum(self.sides, S, C, q[S], k_cache, self.lse, out=self.colsum, stream=stream)
+        token_select(self.sides, S, C, self.sink, self.colsum, self.k_tok, out=self.tsel,
+                     stream=stream)
+        rpS, ciS, capS, G_S, nS = self.tlists_S
+        build_block_lists(self.bh, G_S, nS, [(self.tsel, False)], capS, rpS, ciS, self.status,
+                          stream=stream)
+        token_cache_residual(self.sides, S, C, q[S], k_cache, v_cache, rpS, ciS, out[S],
+                             o_cache=self.o_cache, stream=stream)
+        for k in self.targets:
+            token_map(self.sides, S, k, C, self.sink, self.tsel, self.map_mode, out=self.tmap[k],
+                      stream=stream)
+            rp, ci, cap, G, n = self.tlists[k]
+            build_block_lists(self.bh, G, n, [(self.tmap[k], False)], cap, rp, ci, self.status,
+                              stream=stream)
+            token_sparse_attn_cached(self.sides, k, C, q[k], k_cache, v_cache, rp, ci,
+                                     self.o_cache, S, o=out[k], stream=stream)
 
     def kind(self, layer: int) -> str:
         return "cs4a" if layer < self.n_cs4a else "csla"
@@ -101,7 +153,9 @@ class SparsifiedStep:
     def layer(self, l: int, q: Dict[int, torch.Tensor], k_cache, v_cache,
               out: Dict[int, torch.Tensor], stream=None):
         S, B = self.S, self.B
-        if self.kind(l) == "cs4a":
+        if self.kind(l) == "cs4a" and self.granularity == "token":
+            self._token_cs4a(q, k_cache, v_cache, out, stream)
+        elif self.kind(l) == "cs4a":
             gS = self.gS
             if self.fused:
                 dense_attn_mass(self.sides, S, B, self.sink, q[S], k_cache, v_cache,

@@ -99,6 +99,15 @@ def main():
         st_u.run(qs, ks, vs, outs)
     unfused_ms = timed(lambda: st_u.run(qs, ks, vs, outs), args.steps)
 
+    # CS4A layers at the paper's token granularity (NEXT(2): C = 192, alpha = 0.2)
+    st_t = step.SparsifiedStep(SIDES, S, K, B, bh, L, head_dim=D, topk=5, granularity="token",
+                               query_block=192, alpha=0.2)
+    for _ in range(args.warmup):
+        st_t.run(qs, ks, vs, outs)
+    torch.cuda.synchronize()
+    assert st_t.status.item() == 0
+    token_ms = timed(lambda: st_t.run(qs, ks, vs, outs), args.steps)
+
     # per layer kind (one layer of each, repeated), for the breakdown
     st.csla_patterns()
     lay = {}
@@ -108,6 +117,7 @@ def main():
            "value": round(sparse_ms, 4), "unit": "ms/step", "higher_is_better": False,
            "dense_ms": round(dense_ms, 4), "speedup_vs_dense": round(dense_ms / sparse_ms, 3),
            "unfused_predictor_ms": round(unfused_ms, 4),
+           "token_granularity_ms": round(token_ms, 4),
            "graph_replay_ms": graph_ms if not isinstance(graph_ms, float) else round(graph_ms, 4),
            "layers": L, "cs4a_layers": st.n_cs4a, "csla_layers": L - st.n_cs4a,
            "cs4a_layer_ms": round(lay["cs4a"], 4), "csla_layer_ms": round(lay["csla"], 4),

@@ -99,3 +99,39 @@ def test_run_matches_layerwise(step_mod):
     for l in range(layers):
         for k in a[l]:
             assert torch.equal(a[l][k], b[l][k]), (l, k)
+
+
+def test_token_granularity_step(step_mod):
+    """granularity='token': CS4A layers run the token path (NEXT(2)); every output of a 2-layer
+    (CS4A + CSLA) step against the oracle's token path on the GPU's own selections."""
+    from oracle.token_cs4a import map_tokens, token_cache_residual, token_cached_sparse
+    cfg = EQ256
+    sides, S, K, B, D, sink = cfg["sides"], cfg["S"], cfg["K"], cfg["B"], cfg["D"], cfg["sink"]
+    bh, layers, C = 2, 2, 64
+    sched = Schedule(sides)
+    st = step_mod.SparsifiedStep(sides, S, K, B, bh, layers, head_dim=D, sink_scales=sink,
+                                 windows=cfg["windows"], cs4a_fraction=0.5, granularity="token",
+                                 query_block=C, alpha=0.2)
+    qs = [{k: q_iid(50 + l, k, 0, bh, sched.N(k), D).cuda() for k in range(S, K + 1)}
+          for l in range(layers)]
+    kvs = [kv_cache_iid(50 + l, 0, bh, sched.C(K), D) for l in range(layers)]
+    ks, vs = [k.cuda() for k, _ in kvs], [v.cuda() for _, v in kvs]
+    outs = st.alloc_outputs()
+    st.csla_patterns()
+    st.layer(0, qs[0], ks[0], vs[0], outs[0])
+    torch.cuda.synchronize()
+    assert st.status.item() == 0
+    sel = bits_to_bool(st.tsel.cpu().numpy(), sched.C(S))
+    for b in range(bh):
+        qb = {k: to_np(qs[0][k][b]) for k in range(S, K + 1)}
+        kb, vb = to_np(ks[0][b]), to_np(vs[0][b])
+        mx, mean = attn_errors(to_np(outs[0][S][b]), dense(qb[S], kb, vb, sched.C(S)))
+        assert mx <= MAX_ABS and mean <= MEAN_ABS
+        oc = token_cache_residual(qb[S], kb, vb, sched.C(S), C, sel[b])
+        for k in st.targets:
+            got_map = bits_to_bool(st.tmap[k].cpu().numpy(), sched.C(k))[b]
+            want_map = map_tokens(sel[b], sched, S, k, C, sink)
+            assert np.array_equal(got_map, want_map), k
+            want = token_cached_sparse(qb[k], kb, vb, C, want_map, oc, sides[S - 1], sides[k - 1])
+            mx, mean = attn_errors(to_np(outs[0][k][b]), want)
+            assert mx <= MAX_ABS and mean <= MEAN_ABS, (k, mx, mean)
