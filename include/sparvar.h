@@ -274,6 +274,37 @@ sparvar_status sparvar_token_sparse_attn_cached(
     const uint16_t* o_cache, int32_t cache_scale, int64_t cache_stride_bh, uint16_t* o,
     void* stream);
 
+/* NEXT(4) — compressed KV cache for CSLA layers ("retaining only sinks and local scales KV
+ *   Cache"): a CSLA layer at target K reads only the sink scales (h <= sink_scales)
+ *   and the scales with a window (windows[K - h] > 0); the compressed cache holds those scales'
+ *   rows in scale order (READING 23).
+ * sparvar_csla_kept_rows: its row count (-1 on invalid arguments).
+ * sparvar_compress_kv: copies the kept rows of a full cache (rows C_{h-1}..C_h of every kept h,
+ *   in_stride_bh elements per (b,h)) into cache_out (out_stride_bh >= kept rows * D), on stream.
+ * sparvar_local_mask_compressed: sparvar_local_mask's block mask over the compressed index,
+ *   [G_q][ceil(ceil(kept/block)/32)] words (blocks straddle kept scales as in the full cache).
+ * sparvar_block_sparse_attn_rows: sparvar_block_sparse_attn over a cache of kv_rows valid rows
+ *   (1 <= kv_rows <= C_K), e.g. the compressed cache with the compressed mask's lists.
+ */
+int64_t sparvar_csla_kept_rows(const sparvar_schedule* sched, int32_t target_scale,
+                               int32_t sink_scales, const int32_t* windows, int32_t num_windows);
+sparvar_status sparvar_compress_kv(const sparvar_schedule* sched, int32_t target_scale,
+                                   int32_t sink_scales, const int32_t* windows,
+                                   int32_t num_windows, int32_t batch_heads, int32_t head_dim,
+                                   const uint16_t* cache_in, int64_t in_stride_bh,
+                                   uint16_t* cache_out, int64_t out_stride_bh, void* stream);
+sparvar_status sparvar_local_mask_compressed(const sparvar_schedule* sched, int32_t target_scale,
+                                             int32_t block, int32_t sink_scales,
+                                             const int32_t* windows, int32_t num_windows,
+                                             uint32_t* mask_out, void* stream);
+sparvar_status sparvar_block_sparse_attn_rows(const sparvar_schedule* sched,
+                                              int32_t target_scale, int32_t block,
+                                              const sparvar_attn_shape* shape, const uint16_t* q,
+                                              const uint16_t* k_cache, const uint16_t* v_cache,
+                                              int64_t kv_rows, const int32_t* row_ptr,
+                                              const int32_t* col_idx, float softmax_scale,
+                                              uint16_t* o, float* lse, void* stream);
+
 /* NEXT(1) — cached block-sparse attention at scale K:
  *   O^(K) = Upsample(O_cache) + Delta O^(K), Delta O^(K) = sparvar_block_sparse_attn output.
  *   Upsample is nearest neighbour over the query grid: output query (x, y) of side s_K adds

@@ -24,7 +24,8 @@ __all__ = [
     "build_block_lists", "block_sparse_attn", "dense_attn", "cache_residual",
     "block_sparse_attn_cached", "cache_residual_from_dense", "dense_attn_mass",
     "dense_attn_mass_workspace", "token_colsum", "token_select", "token_map", "token_sparse_attn",
-    "token_cache_residual", "token_sparse_attn_cached",
+    "token_cache_residual", "token_sparse_attn_cached", "csla_kept_rows", "compress_kv",
+    "local_mask_compressed", "block_sparse_attn_rows",
     "SparseLayer", "unpack_bits",
     "SELECT_TOPK", "SELECT_THRESHOLD", "MAP_FOOTPRINT", "MAP_POINT",
 ]
@@ -81,6 +82,9 @@ def _load(path: str = LIB_PATH, partial: bool = False):
         "sparvar_token_map": [S, I32, I32, I32, I32, I32, I32, P, P, P],
         "sparvar_token_sparse_attn": [S, I32, I32, SH, P, P, P, P, P, F32, P, P],
         "sparvar_token_cache_residual": [S, I32, I32, SH, P, P, P, P, P, F32, P, P, P],
+        "sparvar_compress_kv": [S, I32, I32, P, I32, I32, I32, P, I64, P, I64, P],
+        "sparvar_local_mask_compressed": [S, I32, I32, I32, P, I32, P, P],
+        "sparvar_block_sparse_attn_rows": [S, I32, I32, SH, P, P, P, I64, P, P, F32, P, P, P],
         "sparvar_token_sparse_attn_cached": [S, I32, I32, SH, P, P, P, P, P, F32, P, I32, I64, P,
                                              P],
     }
@@ -90,6 +94,9 @@ def _load(path: str = LIB_PATH, partial: bool = False):
         f = getattr(L, name)
         f.argtypes = args
         f.restype = ctypes.c_int
+    if hasattr(L, "sparvar_csla_kept_rows"):
+        L.sparvar_csla_kept_rows.argtypes = [S, I32, I32, P, I32]
+        L.sparvar_csla_kept_rows.restype = ctypes.c_int64
     if hasattr(L, "sparvar_dense_attn_mass_workspace"):
         L.sparvar_dense_attn_mass_workspace.argtypes = [S, I32, I32, I32]
         L.sparvar_dense_attn_mass_workspace.restype = ctypes.c_size_t
@@ -393,6 +400,62 @@ def token_sparse_attn_cached(sides, target: int, C: int, q, k_cache, v_cache, ro
         ctypes.byref(_sched(sides)), target, C, ctypes.byref(sh), _ptr(q), _ptr(k_cache),
         _ptr(v_cache), _ptr(row_ptr), _ptr(col_idx), softmax_scale, _ptr(o_cache), cache_scale,
         cstride, _ptr(o), _stream(stream)))
+    return o
+
+
+# ------------------------------------------------------------------ NEXT(4): compressed KV
+def _win(windows):
+    return (ctypes.c_int32 * max(1, len(windows)))(*[int(x) for x in windows])
+
+
+def csla_kept_rows(sides, target: int, sink_scales: int = 5, windows=(7, 5, 3, 1, 1)) -> int:
+    """Rows of the compressed cache of a CSLA layer at `target` (sink + windowed scales)."""
+    n = int(lib.sparvar_csla_kept_rows(ctypes.byref(_sched(sides)), target, sink_scales,
+                                       _win(windows), len(windows)))
+    if n < 0:
+        raise SparVARError(1, "invalid arguments")
+    return n
+
+
+def compress_kv(sides, target: int, cache, sink_scales: int = 5, windows=(7, 5, 3, 1, 1),
+                out=None, stream=None):
+    """(bh, >= C_K, D) bf16 cache -> (bh, kept, D): the CSLA layer's sink + local scales."""
+    bh, _, D = cache.shape
+    kept = csla_kept_rows(sides, target, sink_scales, windows)
+    if out is None:
+        out = torch.empty((bh, kept, D), dtype=cache.dtype, device=cache.device)
+    _check(lib.sparvar_compress_kv(ctypes.byref(_sched(sides)), target, sink_scales, _win(windows),
+                                   len(windows), bh, D, _ptr(cache), _bh_view(cache, "cache"),
+                                   _ptr(out), _bh_view(out, "out"), _stream(stream)))
+    return out
+
+
+def local_mask_compressed(sides, target: int, block: int, sink_scales: int = 5,
+                          windows=(7, 5, 3, 1, 1), out=None, stream=None):
+    kept = csla_kept_rows(sides, target, sink_scales, windows)
+    g_q = -(-(sides[target - 1] ** 2) // block)
+    W = -(-(-(-kept // block)) // 32)
+    if out is None:
+        out = torch.empty((g_q, W), dtype=torch.int32, device="cuda")
+    _check(lib.sparvar_local_mask_compressed(ctypes.byref(_sched(sides)), target, block, sink_scales,
+                                             _win(windows), len(windows), _ptr(out),
+                                             _stream(stream)))
+    return out
+
+
+def block_sparse_attn_rows(sides, target: int, block: int, q, k_cache, v_cache, kv_rows: int,
+                           row_ptr, col_idx, softmax_scale: float = 0.0, o=None, lse=None,
+                           stream=None):
+    """block_sparse_attn over a cache with kv_rows valid rows (e.g. the compressed cache)."""
+    if o is None:
+        o = torch.empty_like(q)
+    if _bh_view(v_cache, "v_cache") != k_cache.stride(0):
+        raise ValueError("k_cache and v_cache must share a (b,h) stride")
+    sh = _attn_shape(q, k_cache, o)
+    _check(lib.sparvar_block_sparse_attn_rows(ctypes.byref(_sched(sides)), target, block,
+                                              ctypes.byref(sh), _ptr(q), _ptr(k_cache),
+                                              _ptr(v_cache), kv_rows, _ptr(row_ptr), _ptr(col_idx),
+                                              softmax_scale, _ptr(o), _ptr(lse), _stream(stream)))
     return o
 
 

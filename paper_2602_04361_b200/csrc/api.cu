@@ -122,7 +122,7 @@ extern "C" {
 
 const char* sparvar_last_error(void) { return g_err.c_str(); }
 
-int32_t sparvar_version(void) { return 104; }   // 1.04: + token-level CS4A with O_cache (NEXT(2))
+int32_t sparvar_version(void) { return 105; }   // 1.05: + compressed KV for CSLA layers (NEXT(4))
 
 sparvar_status sparvar_local_mask(const sparvar_schedule* sched, int32_t target_scale,
                                   int32_t block, int32_t sink_scales, const int32_t* windows,
@@ -149,6 +149,94 @@ sparvar_status sparvar_local_mask(const sparvar_schedule* sched, int32_t target_
   if (e == cudaErrorInvalidValue)
     return fail(SPARVAR_ERR_UNSUPPORTED, "mask row too wide for shared memory");
   if (e != cudaSuccess) return cuda_fail(e, "local_mask launch");
+  return ok();
+}
+
+// ---------------------------------------------------------------- NEXT(4): compressed KV
+static sparvar_status csla_windows(const int32_t* windows, int32_t num_windows, int* rel) {
+  if (num_windows < 0 || num_windows > sv::kMaxScales || (num_windows > 0 && windows == nullptr))
+    return fail(SPARVAR_ERR_INVALID_ARG, "bad windows array");
+  for (int i = 0; i < sv::kMaxScales; ++i) rel[i] = 0;
+  for (int i = 0; i < num_windows; ++i) {
+    if (windows[i] < 0 || (windows[i] > 0 && windows[i] % 2 == 0))
+      return fail(SPARVAR_ERR_INVALID_ARG, "window %d must be 0 or odd", windows[i]);
+    rel[i] = windows[i];
+  }
+  return SPARVAR_OK;
+}
+
+int64_t sparvar_csla_kept_rows(const sparvar_schedule* sched, int32_t target_scale,
+                               int32_t sink_scales, const int32_t* windows, int32_t num_windows) {
+  sv::Geo g;
+  int rel[sv::kMaxScales];
+  if (make_geo(sched, &g) != SPARVAR_OK || target_scale < 1 || target_scale > g.K ||
+      csla_windows(windows, num_windows, rel) != SPARVAR_OK)
+    return -1;
+  long long n = 0;
+  for (int h = 1; h <= target_scale; ++h)
+    if (h <= sink_scales || rel[target_scale - h] > 0) n += (long long)g.side[h - 1] * g.side[h - 1];
+  return n;
+}
+
+sparvar_status sparvar_local_mask_compressed(const sparvar_schedule* sched, int32_t target_scale,
+                                             int32_t block, int32_t sink_scales,
+                                             const int32_t* windows, int32_t num_windows,
+                                             uint32_t* mask_out, void* stream) {
+  sv::Geo g;
+  sparvar_status s = make_geo(sched, &g);
+  if (s != SPARVAR_OK) return s;
+  if (target_scale < 1 || target_scale > g.K)
+    return fail(SPARVAR_ERR_INVALID_ARG, "target_scale %d not in [1, %d]", target_scale, g.K);
+  if (block < 1) return fail(SPARVAR_ERR_INVALID_ARG, "block %d < 1", block);
+  if (sink_scales < 0 || sink_scales > target_scale)
+    return fail(SPARVAR_ERR_INVALID_ARG, "sink_scales %d not in [0, %d]", sink_scales, target_scale);
+  int rel[sv::kMaxScales];
+  if ((s = csla_windows(windows, num_windows, rel)) != SPARVAR_OK) return s;
+  if (mask_out == nullptr) return fail(SPARVAR_ERR_INVALID_ARG, "null mask_out");
+  cudaError_t e = sv::launch_local_mask(g, target_scale, block, sink_scales, rel, mask_out,
+                                        (cudaStream_t)stream, true);
+  if (e == cudaErrorInvalidValue)
+    return fail(SPARVAR_ERR_UNSUPPORTED, "mask row too wide for shared memory");
+  if (e != cudaSuccess) return cuda_fail(e, "local_mask launch");
+  return ok();
+}
+
+sparvar_status sparvar_compress_kv(const sparvar_schedule* sched, int32_t target_scale,
+                                   int32_t sink_scales, const int32_t* windows,
+                                   int32_t num_windows, int32_t batch_heads, int32_t head_dim,
+                                   const uint16_t* cache_in, int64_t in_stride_bh,
+                                   uint16_t* cache_out, int64_t out_stride_bh, void* stream) {
+  sv::Geo g;
+  sparvar_status s = make_geo(sched, &g);
+  if (s != SPARVAR_OK) return s;
+  if (target_scale < 1 || target_scale > g.K)
+    return fail(SPARVAR_ERR_INVALID_ARG, "target_scale %d not in [1, %d]", target_scale, g.K);
+  if (sink_scales < 0 || sink_scales > target_scale)
+    return fail(SPARVAR_ERR_INVALID_ARG, "sink_scales %d not in [0, %d]", sink_scales, target_scale);
+  int rel[sv::kMaxScales];
+  if ((s = csla_windows(windows, num_windows, rel)) != SPARVAR_OK) return s;
+  if (batch_heads < 1 || (head_dim != 64 && head_dim != 128))
+    return fail(SPARVAR_ERR_INVALID_ARG, "batch_heads %d / head_dim %d", batch_heads, head_dim);
+  if (cache_in == nullptr || cache_out == nullptr) return fail(SPARVAR_ERR_INVALID_ARG, "null cache");
+  const long long kept = sparvar_csla_kept_rows(sched, target_scale, sink_scales, windows, num_windows);
+  if (in_stride_bh < (long long)g.cum[target_scale] * head_dim || out_stride_bh < kept * head_dim)
+    return fail(SPARVAR_ERR_INVALID_ARG, "stride too small for the (compressed) cache");
+  // one 2-D copy (rows of every (b,h)) per maximal run of kept scales
+  long long dst_row = 0;
+  for (int h = 1; h <= target_scale;) {
+    const bool keep = h <= sink_scales || rel[target_scale - h] > 0;
+    if (!keep) { ++h; continue; }
+    int h1 = h;
+    while (h1 + 1 <= target_scale && (h1 + 1 <= sink_scales || rel[target_scale - h1 - 1] > 0)) ++h1;
+    const long long r0 = g.cum[h - 1], rows = g.cum[h1] - g.cum[h - 1];
+    cudaError_t e = cudaMemcpy2DAsync(cache_out + dst_row * head_dim, out_stride_bh * 2,
+                                      cache_in + r0 * head_dim, in_stride_bh * 2,
+                                      rows * head_dim * 2, batch_heads, cudaMemcpyDeviceToDevice,
+                                      (cudaStream_t)stream);
+    if (e != cudaSuccess) return cuda_fail(e, "compress copy");
+    dst_row += rows;
+    h = h1 + 1;
+  }
   return ok();
 }
 
@@ -266,7 +354,7 @@ static sparvar_status attn_common(const sparvar_schedule* sched, int32_t target_
                                   uint16_t* o, float* lse, void* stream,
                                   const uint16_t* add = nullptr, int32_t add_scale = 0,
                                   int64_t add_stride = 0, float* mass_s = nullptr,
-                                  float* mass_m = nullptr) {
+                                  float* mass_m = nullptr, long long n_kv_rows = -1) {
   sv::Geo g;
   sparvar_status s = make_geo(sched, &g);
   if (s != SPARVAR_OK) return s;
@@ -275,7 +363,9 @@ static sparvar_status attn_common(const sparvar_schedule* sched, int32_t target_
   if (!attn_block_ok(block))
     return fail(SPARVAR_ERR_UNSUPPORTED, "block %d not in {16, 32, 64, 128}", block);
   const long long n_q = (long long)g.side[target_scale - 1] * g.side[target_scale - 1];
-  const long long n_kv = g.cum[target_scale];
+  const long long n_kv = n_kv_rows >= 0 ? n_kv_rows : g.cum[target_scale];
+  if (n_kv < 1 || n_kv > g.cum[target_scale])
+    return fail(SPARVAR_ERR_INVALID_ARG, "kv rows %lld not in [1, C_K]", n_kv);
   s = check_shape(shape, n_q, n_kv, true);
   if (s != SPARVAR_OK) return s;
   if (q == nullptr || k == nullptr || v == nullptr || o == nullptr)
@@ -624,6 +714,19 @@ sparvar_status sparvar_block_sparse_attn_cached(
                 "and o_cache 16-byte aligned");
   return attn_common(sched, target_scale, block, shape, q, k_cache, v_cache, row_ptr, col_idx,
                      softmax_scale, o, lse, stream, o_cache, cache_scale, cache_stride_bh);
+}
+
+sparvar_status sparvar_block_sparse_attn_rows(const sparvar_schedule* sched,
+                                              int32_t target_scale, int32_t block,
+                                              const sparvar_attn_shape* shape, const uint16_t* q,
+                                              const uint16_t* k_cache, const uint16_t* v_cache,
+                                              int64_t kv_rows, const int32_t* row_ptr,
+                                              const int32_t* col_idx, float softmax_scale,
+                                              uint16_t* o, float* lse, void* stream) {
+  if (row_ptr == nullptr || col_idx == nullptr)
+    return fail(SPARVAR_ERR_INVALID_ARG, "null row_ptr / col_idx");
+  return attn_common(sched, target_scale, block, shape, q, k_cache, v_cache, row_ptr, col_idx,
+                     softmax_scale, o, lse, stream, nullptr, 0, 0, nullptr, nullptr, kv_rows);
 }
 
 sparvar_status sparvar_dense_attn(const sparvar_schedule* sched, int32_t target_scale,

@@ -19,7 +19,7 @@ struct Geo {
 // ------------------------------------------------------------------ masks.cu
 cudaError_t launch_local_mask(const Geo& g, int target, int block, int sink_scales,
                               const int* windows_rel /*[kMaxScales], index = target - h*/,
-                              uint32_t* out, cudaStream_t st);
+                              uint32_t* out, cudaStream_t st, bool compressed = false);
 cudaError_t launch_map_indices(const Geo& g, int S, int K, int block, int sink_scales, int mode,
                                int bh, const uint32_t* src, uint32_t* dst, cudaStream_t st);
 struct MaskSet {

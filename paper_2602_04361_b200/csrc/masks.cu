@@ -43,6 +43,8 @@ __device__ __forceinline__ void set_token_range(uint32_t* row, int t0, int t1, i
 // the blocks each square row covers.  The sink prefix [0, C_sink) is a single range.
 struct WinArr {
   int w[kMaxScales];   // w[i] = window of scale K - i
+  int base[kMaxScales];  // first cache row of scale h at [h-1]: C_{h-1}, or the compressed
+                         // offset when the cache keeps only the CSLA scales (NEXT(4))
 };
 
 __global__ void local_mask_kernel(const Geo g, int K, int B, int sink_scales, const WinArr win,
@@ -65,7 +67,7 @@ __global__ void local_mask_kernel(const Geo g, int K, int B, int sink_scales, co
       const int yt = min(rne_div((long long)y * sh, sK), sh - 1);
       const int x0 = max(0, xt - r), x1 = min(sh - 1, xt + r);
       const int y0 = max(0, yt - r), y1 = min(sh - 1, yt + r);
-      const int base = g.cum[h - 1];
+      const int base = win.base[h - 1];
       for (int xr = x0; xr <= x1; ++xr)
         set_token_range(srow, base + xr * sh + y0, base + xr * sh + y1, B);
     }
@@ -526,12 +528,21 @@ __global__ void __launch_bounds__(256) wide_write_kernel(int g_q, int W, MaskSet
 }  // namespace
 
 cudaError_t launch_local_mask(const Geo& g, int target, int block, int sink_scales,
-                              const int* windows_rel, uint32_t* out, cudaStream_t st) {
+                              const int* windows_rel, uint32_t* out, cudaStream_t st,
+                              bool compressed) {
   WinArr win;
   for (int i = 0; i < kMaxScales; ++i) win.w[i] = windows_rel[i];
+  // compressed cache (NEXT(4)): only the sink scales and the windowed scales, in scale order
+  int n_kv = 0;
+  for (int h = 1; h <= target; ++h) {
+    const bool keep = !compressed || h <= sink_scales || windows_rel[target - h] > 0;
+    win.base[h - 1] = compressed ? n_kv : g.cum[h - 1];
+    if (keep) n_kv += g.side[h - 1] * g.side[h - 1];
+  }
+  if (!compressed) n_kv = g.cum[target];
   const int nq = g.side[target - 1] * g.side[target - 1];
   const int gq = (nq + block - 1) / block;
-  const int gkv = (g.cum[target] + block - 1) / block;
+  const int gkv = (n_kv + block - 1) / block;
   const int W = (gkv + 31) / 32;
   const size_t smem = size_t(W) * 4;
   if (smem > 200 * 1024) return cudaErrorInvalidValue;

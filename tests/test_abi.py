@@ -25,14 +25,14 @@ def _declared():
 
 def test_exports_every_declared_symbol(sv):
     names = _declared()
-    assert "sparvar_block_sparse_attn" in names and len(names) == 19
+    assert "sparvar_block_sparse_attn" in names and len(names) == 23
     L = ctypes.CDLL(sv.LIB_PATH)
     for n in names:
         assert hasattr(L, n), n
 
 
 def test_version_and_error_string(sv):
-    assert sv.lib.sparvar_version() == 104
+    assert sv.lib.sparvar_version() == 105
     assert isinstance(sv.lib.sparvar_last_error(), bytes)
 
 
