@@ -30,8 +30,18 @@ except Exception:
     clk = lambda: -1
 res = {(n, w): [] for n in handles for w in nnz}
 clks = []
-for rep in range(7):
-    for name, L in handles.items():
+import random
+import time
+rng = random.Random(1234)
+names = list(handles)
+for rep in range(9):
+    # random order per round and a short idle gap before each library: no position bias from
+    # the power / clock state the previous library left behind
+    order = names[:]
+    rng.shuffle(order)
+    for name in order:
+        L = handles[name]
+        time.sleep(0.05)
         sv.lib = L
         for w in ("csla", "cs4a", "dense"):
             fn = (lambda: sv.dense_attn(sides, K, q, k, v)) if w == "dense" else \
@@ -47,12 +57,12 @@ for rep in range(7):
             torch.cuda.synchronize()
             clks.append(clk())
             res[(name, w)].append(e0.elapsed_time(e1) / reps)
-print("SM clock MHz during runs: median %s min %s  (times: min over 7 interleaved rounds)" % (statistics.median(clks), min(clks)))
+print("SM clock MHz during runs: median %s min %s  (times: median [min] over 9 rounds, shuffled order)" % (statistics.median(clks), min(clks)))
 for name in handles:
     line = [name.ljust(18)]
     for w in ("csla", "cs4a", "dense"):
-        ms = min(res[(name, w)])
-        line.append(f"{w} {ms:.4f} ms ({4 * D * B * B * nnz[w] / ms / 1e9:.0f} TF)")
-    d, c = min(res[(name, "dense")]), min(res[(name, "csla")])
+        ms = statistics.median(res[(name, w)])
+        line.append(f"{w} {ms:.4f} [{min(res[(name, w)]):.4f}] ms ({4 * D * B * B * nnz[w] / ms / 1e9:.0f} TF)")
+    d, c = statistics.median(res[(name, "dense")]), statistics.median(res[(name, "csla")])
     line.append(f"x{d / c:.2f}")
     print("  ".join(line), flush=True)
