@@ -1,5 +1,7 @@
-# ncu evidence for the NEXT(2) token kernels and the NEXT(3) fused pass (run under gpurun; 1 GPU)
+# ncu evidence for the NEXT(2) token kernels (run under gpurun; 1 GPU): one full-set capture each
 python -c "import __graft_entry__ as g; g.build()"
-ncu --set full --import-source on --clock-control none -k regex:"colsum_kernel|token_attn_kernel|topk_tokens|map_tokens" -c 4 \
-    -o gpurun_out/token_full -f python scripts/token_bench.py --reps 1 > gpurun_out/ncu_token.log 2>&1
-tail -2 gpurun_out/ncu_token.log
+for k in colsum_kernel token_attn_kernel topk_tokens_kernel map_tokens_kernel; do
+  ncu --set full --import-source on --clock-control none -k regex:$k -s 1 -c 1 \
+      -o gpurun_out/tok_$k -f python scripts/token_bench.py --reps 1 > gpurun_out/ncu_$k.log 2>&1
+  tail -1 gpurun_out/ncu_$k.log
+done

@@ -1,4 +1,5 @@
-"""Development aid: blocked-clock breakdown of the column-split predictor (SV_PRED_PROF build).
+"""Development aid: blocked-clock breakdown of the column-split predictor (SV_PRED_PROF build of
+experiments/predictor_column_split.cu.txt copied over csrc/predictor.cu).
     SPARVAR_LIB=variants/lib_pprof.so python scripts/pred_prof.py"""
 import ctypes
 import os
