@@ -100,10 +100,11 @@ constexpr int ORDER = SV_ORDER;
 #define SV_LEAN 1      // lean MMA issue loop (one P wait per op, no warp syncs)
 #endif
 #ifndef SV_MMA_POLL
-#define SV_MMA_POLL 0
+#define SV_MMA_POLL 1
 #endif
 // The MMA issuer polls its barriers (mbarrier.test_wait) instead of try_wait, which may
-// suspend the thread: a suspended issuer wakes late and leaves the tensor pipe idle.
+// suspend the thread: a suspended issuer wakes late and leaves the tensor pipe idle (-2.3% CSLA
+// time in shuffled-order timing; polling in the K/V loader or the softmax warps gains nothing).
 #if SV_MMA_POLL
 #define SV_MMA_WAIT mbar_wait_spin
 #elif SV_MMA_DBG
