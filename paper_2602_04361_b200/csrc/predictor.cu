@@ -17,7 +17,7 @@
 //    than 2^8).  At the tile end each row normalises by l = sum of its block sums (exact:
 //    P[q, j] = 2^(s' - m) / l), rows are reduced per query block in a fixed order
 //    (deterministic), and one warp per query block selects with ballots into bit rows.
-//  * A fraction of the exp2 runs as a degree-4 polynomial on the FMA pipe (relative error
+//  * One in eight exp2 pairs runs as a degree-4 polynomial on the FMA pipe (relative error
 //    2.6e-6, well inside the 1e-4 mass tolerance) to take load off the MUFU pipe.
 #include <cuda_bf16.h>
 #include <cstdio>
@@ -31,7 +31,7 @@
 #define SV_PRED_QB 4     // preferred number of Q buffers (2..4); fewer if shared memory is short
 #endif
 #ifndef SV_PRED_EMU_EVERY
-#define SV_PRED_EMU_EVERY 4   // 1 in 4 exp2 pairs as a degree-4 polynomial on the FMA pipe (-3%)
+#define SV_PRED_EMU_EVERY 8   // 1 in 8 exp2 pairs as a degree-4 polynomial on the FMA pipe
 #endif
 
 namespace sv {
