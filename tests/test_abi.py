@@ -105,3 +105,42 @@ def test_no_fallback_when_library_missing(tmp_path, monkeypatch):
     mod = importlib.util.module_from_spec(spec)
     with pytest.raises(ImportError):
         spec.loader.exec_module(mod)
+
+
+def test_next_rows_validation(sv):
+    """Host-side validation of the NEXT(1)-(4) entry points (no device work is reached)."""
+    p = ctypes.c_void_p(256)
+    S4 = _sched(sv, [1, 2, 4, 8])
+    sh = sv._Shape(1, 64, 64 * 64, 85 * 64, 64 * 64)
+    # token path: query_block outside {64, 128, 192}
+    st = sv.lib.sparvar_token_colsum(S4, 3, 100, ctypes.byref(sh), p, p, p, 0.0, p, None)
+    assert st == 3 and b"query_block" in sv.lib.sparvar_last_error()
+    st = sv.lib.sparvar_token_sparse_attn(S4, 4, 96, ctypes.byref(sh), p, p, p, p, p, 0.0, p, None)
+    assert st == 3
+    st = sv.lib.sparvar_token_select(S4, 3, 64, 0, 1, p, 0, p, None)      # topk_tokens < 1
+    assert st == 1
+    st = sv.lib.sparvar_token_map(S4, 4, 3, 64, 0, 0, 1, p, p, None)      # src > dst
+    assert st == 1
+    # cached paths: cache_scale above the target, o_dense aliasing o_cache
+    st = sv.lib.sparvar_token_sparse_attn_cached(S4, 3, 64, ctypes.byref(sh), p, p, p, p, p, 0.0,
+                                                 p, 4, 64 * 64, p, None)
+    assert st == 1
+    st = sv.lib.sparvar_cache_residual_from_dense(S4, 3, 16, ctypes.byref(sh), p, p, p, p, p, 0.0,
+                                                  p, p, None)
+    assert st == 1 and b"alias" in sv.lib.sparvar_last_error()
+    # fused dense + mass: workspace too small -> CAPACITY before any launch
+    need = sv.lib.sparvar_dense_attn_mass_workspace(S4, 3, 16, 1)
+    assert need > 0
+    st = sv.lib.sparvar_dense_attn_mass(S4, 3, 16, 1, ctypes.byref(sh), p, p, p, 0.0, 0, 2, 0.0,
+                                        p, None, None, p, p, need - 16, None)
+    assert st == 4
+    # compressed KV: kept rows and window validation
+    w = (ctypes.c_int32 * 2)(3, 1)
+    assert sv.lib.sparvar_csla_kept_rows(S4, 4, 1, w, 2) == 1 + 16 + 64
+    bad = (ctypes.c_int32 * 1)(2)
+    assert sv.lib.sparvar_csla_kept_rows(S4, 4, 1, bad, 1) == -1
+    st = sv.lib.sparvar_local_mask_compressed(S4, 4, 16, 1, bad, 1, p, None)
+    assert st == 1 and b"odd" in sv.lib.sparvar_last_error()
+    st = sv.lib.sparvar_block_sparse_attn_rows(S4, 4, 16, ctypes.byref(sh), p, p, p, 86, p, p, 0.0,
+                                               p, None, None)   # more rows than C_K = 85
+    assert st == 1
