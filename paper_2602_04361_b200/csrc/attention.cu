@@ -6,14 +6,17 @@
 //
 // Design (DESIGN.md §7 "attn_fwd_kernel"):
 //  * Persistent, one CTA per SM (all 512 TMEM columns).  The 128-row query tiles ("items",
-//    (b,h)-major) are split into CONTIGUOUS per-CTA ranges of equal cost (cost = listed blocks +
-//    a per-tile overhead), found by a warp-parallel search over row_ptr (the CSR prefix sums).
+//    (b,h)-major) are dealt in strided windows: CTA c takes position (c + 59 k) mod grid of the
+//    k-th window of `grid` consecutive items, so at any time the grid works on a few heads whose
+//    K/V stay in L2 (SV_ORDER=0: cost-balanced contiguous ranges found by a warp-parallel search
+//    over row_ptr).
 //  * Two tile SLOTS per CTA, each with its own S/P (128 TMEM cols) and O (D cols) accumulators
 //    and its own softmax warpgroup: the tensor core works on one slot while the other slot's
 //    softmax runs.  The MMA warp issues in a fixed round-robin order (per round and slot:
-//    O += P_j V_j in two halves, then S = Q K_{j+1}^T or the next tile's first S), and every role
-//    derives the same order from a per-CTA schedule (thread 0 simulates the round-robin once per
-//    batch of up to MAX_TILES tiles), so one KV ring serves both slots.
+//    O += P_j V_j once all of P is written, then S = Q K_{j+1}^T or the next tile's first S), and
+//    every role derives the same order from a per-CTA schedule (thread 0 simulates the
+//    round-robin once per batch of up to MAX_TILES tiles), so one KV ring serves both slots.
+//    The issuer polls its barriers (a suspended try_wait wakes late and idles the tensor pipe).
 //  * Q lives in 3 shared buffers (two current tiles + one prefetched); a buffer is released by
 //    the commit of its tile's last Q K^T and the schedule gives each new tile the earliest
 //    pending release (that release precedes the tile's first MMA, so no deadlock).
@@ -23,7 +26,11 @@
 //    max grows by more than 2^8); the S_j commit also covers P_{j-1} V_{j-1}.
 //  * A separate epilogue warpgroup drains each finished tile (TMEM O -> 1/l -> bf16 -> global,
 //    LSE) in completion order, so the softmax warpgroup starts the slot's next tile at once; the
-//    next tile's first P.V waits on "O drained".
+//    next tile's first P.V waits on "O drained".  Q loads and O stores carry an L2 evict-first
+//    policy (read / written once), K/V loads evict-last (re-read by other tiles of the head).
+//  * MASS instantiation (NEXT(3), sparvar_dense_attn_mass): the softmax warps also store each
+//    step's block sum and reference max for the fused predictor (mass_select_kernel).
+//  * NEXT(1): an optional NN-upsampled residual is added in the epilogue.
 //  * Block sizes below 128: a 128-row tile holds G = 128/B query blocks; the KV steps are the
 //    ascending union of their lists and each row masks the steps its own block does not list.
 //    The ragged last KV block is masked to -inf (READING 20): TMA zero fill alone gives logit 0.
