@@ -7,8 +7,9 @@ collective.  Inputs are regenerated per rank from the counter-based generator in
 single-process run bit for bit.  The only collectives are off the timed path:
 
   * `max_over_ranks`: per-rank device times -> the job time (max over ranks);
-  * `gather_to_root`: sampled output rows of every rank -> rank 0, for validation against the
-    oracle (all_gather_into_tensor over NCCL on the GPU box; gloo in the CPU tests).
+  * `gather_to_root`: sampled output rows of every rank -> rank 0, for validation (bench.py
+    compares them with the kernel re-run on rank 0; all_gather_into_tensor over NCCL on the GPU
+    box; gloo in the CPU tests).
 """
 from __future__ import annotations
 
