@@ -34,7 +34,7 @@ import random
 import time
 rng = random.Random(1234)
 names = list(handles)
-for rep in range(9):
+for rep in range(int(os.environ.get("SV_ROUNDS", "9"))):
     # random order per round and a short idle gap before each library: no position bias from
     # the power / clock state the previous library left behind
     order = names[:]
@@ -57,7 +57,7 @@ for rep in range(9):
             torch.cuda.synchronize()
             clks.append(clk())
             res[(name, w)].append(e0.elapsed_time(e1) / reps)
-print("SM clock MHz during runs: median %s min %s  (times: median [min] over 9 rounds, shuffled order)" % (statistics.median(clks), min(clks)))
+print("SM clock MHz during runs: median %s min %s  (times: median [min] over %d rounds, shuffled order)" % (statistics.median(clks), min(clks), len(res[next(iter(res))])))
 for name in handles:
     line = [name.ljust(18)]
     for w in ("csla", "cs4a", "dense"):
