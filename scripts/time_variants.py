@@ -10,7 +10,7 @@ import paper_2602_04361_b200 as sv
 libs = sys.argv[1:] or [sv.LIB_PATH]
 handles = {os.path.basename(p): sv._load(os.path.abspath(p), partial=True) for p in libs}
 sides = [1, 2, 4, 6, 8, 12, 16, 20, 24, 32, 40, 48, 64]
-K, S, B, D, bh = 13, 11, 128, 128, 96
+K, S, B, D, bh = 13, 11, 128, 128, int(os.environ.get("SV_BH", "96"))
 torch.manual_seed(0)
 q = torch.randn(bh, 4096, D, device="cuda").bfloat16()
 qS = torch.randn(bh, 1600, D, device="cuda").bfloat16()
