@@ -127,3 +127,36 @@ def test_token_cache_path(sv, sides, S, K, C, D, bh, sink, alpha):
                                    sides[K - 1])
         mx, mean = attn_errors(to_np(o2[b]), want)
         assert mx <= MAX_ABS and mean <= MEAN_ABS, ("O^(K)", b, mx, mean)
+
+
+def test_token_attn_empty_and_ragged_lists(sv):
+    """Hand-built token lists: an empty list gives zero rows (and the cache row when cached), a
+    list of 1 token returns that token's value row, a 130-token list spans a ragged second chunk."""
+    sides, K, C, D, bh = [1, 2, 4, 6, 8, 12, 16], 7, 64, 128, 1
+    sched = Schedule(sides)
+    q = q_iid(61, K, 0, bh, sched.N(K), D).cuda()
+    k, v = kv_cache_iid(61, 0, bh, sched.C(K), D)
+    k, v = k.cuda(), v.cuda()
+    G = ceil_div(sched.N(K), C)                      # 4 query blocks of 64 rows
+    rng = np.random.default_rng(3)
+    lists = [np.array([], dtype=np.int64), np.array([17]),
+             np.sort(rng.choice(sched.C(K), 130, replace=False)),
+             np.sort(rng.choice(sched.C(K), 300, replace=False))]
+    rp = torch.tensor(np.concatenate([[0], np.cumsum([len(x) for x in lists])]), dtype=torch.int32,
+                      device="cuda")
+    ci = torch.tensor(np.concatenate(lists), dtype=torch.int32, device="cuda")
+    o = sv.token_sparse_attn(sides, K, C, q, k, v, rp, ci)
+    oc = torch.randn(bh, sched.N(5), D, device="cuda").bfloat16()
+    o2 = sv.token_sparse_attn_cached(sides, K, C, q, k, v, rp, ci, oc, 5)
+    torch.cuda.synchronize()
+    assert torch.count_nonzero(o[0, :C]) == 0
+    from oracle.cache import upsample_nn
+    up = upsample_nn(to_np(oc[0]), sides[4], sides[K - 1])
+    assert np.abs(to_np(o2[0, :C]) - up[:C]).max() == 0.0          # empty list: the cache row
+    assert torch.equal(o[0, C:2 * C], v[0, 17].unsqueeze(0).expand(C, D))
+    sel = np.zeros((G, sched.C(K)), dtype=bool)
+    for g, l in enumerate(lists):
+        sel[g, l] = True
+    want = token_sparse(to_np(q[0]), to_np(k[0]), to_np(v[0]), C, sel, rows=[2, 3])
+    mx, mean = attn_errors(to_np(o[0])[2 * C:], want[2 * C:])
+    assert mx <= MAX_ABS and mean <= MEAN_ABS, (mx, mean)
