@@ -18,8 +18,9 @@ CASES = [  # sides, K, B, sink, windows, bh, D
     (list(INFINITY_1K_SIDES), 13, 128, 5, (7, 5, 3, 1, 1), 2, 128),
     (list(INFINITY_1K_SIDES), 11, 64, 5, (7, 5, 3, 1, 1), 2, 128),
     ([1, 2, 4, 8, 16], 5, 16, 1, (3, 1), 2, 64),
+    ([1, 2, 4, 6, 8, 12, 16], 7, 16, 0, (5, 0, 3), 2, 128),      # no sink, a masked gap scale
 ]
-IDS = ["256eq", "infinity_K13", "infinity_K11_B64", "d64"]
+IDS = ["256eq", "infinity_K13", "infinity_K11_B64", "d64", "nosink_gap"]
 
 
 @pytest.fixture(scope="module")
