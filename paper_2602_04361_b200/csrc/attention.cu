@@ -103,15 +103,6 @@ constexpr uint8_t EMPTY_TILE = 0xFF;
 // on ~grid consecutive items (a few heads, L2-resident K/V); CTA c takes position
 // (c + k*R) mod grid of window k so a CTA does not keep drawing the same query-tile index.
 constexpr int ORDER = SV_ORDER;
-#ifndef SV_TAIL_LPT
-#define SV_TAIL_LPT 0
-#endif
-// ORDER 1, partial last window: SV_TAIL_LPT=1 deals its items longest-first to the CTAs with the
-// least cost in the full windows (LPT; ranks with ties to the smaller index, identical in every
-// CTA).  On the 8B CSLA lists the static max/mean CTA cost drops from 1.029 to 1.013, but in
-// shuffled-order timing CSLA ran 1.2% slower, CS4A 1.1% faster, dense 1% slower (a few us of
-// set-up per CTA): not adopted; the default keeps the rotated tail.
-constexpr bool TAIL_LPT = SV_TAIL_LPT != 0;
 #ifndef SV_LEAN
 #define SV_LEAN 1      // lean MMA issue loop (one P wait per op, no warp syncs)
 #endif
@@ -291,15 +282,6 @@ __device__ __forceinline__ long long cost_prefix(const AttnArgs& a, int item_beg
   return (long long)(__ldg(a.row_ptr + row) - base_row) + (long long)TILE_OVERHEAD * i;
 }
 
-// Cost of one item (tile): its listed blocks (summed over its G query blocks) + TILE_OVERHEAD.
-template <int G>
-__device__ __forceinline__ int item_cost(const AttnArgs& a, int item, int n_tiles, int g_kv) {
-  if (a.row_ptr == nullptr) return g_kv + TILE_OVERHEAD;
-  const int bh = item / n_tiles, tile = item % n_tiles;
-  const int r0 = bh * a.g_q + min(tile * G, a.g_q), r1 = bh * a.g_q + min((tile + 1) * G, a.g_q);
-  return __ldg(a.row_ptr + r1) - __ldg(a.row_ptr + r0) + TILE_OVERHEAD;
-}
-
 // MASS (NEXT(3), decision-scale dense pass with fused block mass): every softmax thread also
 // stores, per KV step (= key block v), its row's block sum sum_{j in v} 2^(x_j - m) and the m it
 // is relative to (exp2 domain), for mass_select_kernel to normalise with the row's final LSE.
@@ -415,53 +397,12 @@ attn_fwd_kernel(const __grid_constant__ CUtensorMap tmap_q,
   int rot = 59;
   while (gcd_int(rot % grid, grid) != 1 && grid > 1) rot += 2;
   const int k_full = N_items / grid;
-  const int n_rem = N_items - k_full * grid;
-  int tail_item = -1;              // ORDER 1: this CTA's item of the partial last window
-  if (ORDER == 1 && n_rem > 0) {
-    if (TAIL_LPT && grid <= NUM_THREADS) {
-      // scratch in the (not yet loaded) Q buffers: acc[grid], rem cost[n_rem], result
-      int* acc = reinterpret_cast<int*>(sQ);
-      int* rc = acc + grid;
-      int* res = rc + n_rem;
-      for (int i = threadIdx.x; i < grid; i += NUM_THREADS) acc[i] = 0;
-      if (threadIdx.x == 0) *res = -1;
-      __syncthreads();
-      for (int idx = threadIdx.x; idx < N_items; idx += NUM_THREADS) {
-        const int li = idx / grid, p = idx % grid;
-        const int c = item_cost<G>(a, item_begin + idx, n_tiles, g_kv);
-        if (li < k_full)
-          atomicAdd(&acc[(int)(((long long)p - (long long)li * rot % grid + grid) % grid)], c);
-        else
-          rc[p] = c;
-      }
-      __syncthreads();
-      const int me = blockIdx.x, am = acc[me];
-      const int t = threadIdx.x;
-      const int my_rank =
-          __syncthreads_count(t < grid && (acc[t] < am || (acc[t] == am && t < me)));
-      if (my_rank < n_rem) {
-        for (int j = threadIdx.x; j < n_rem; j += NUM_THREADS) {
-          const int cj = rc[j];
-          int r = 0;
-          for (int i = 0; i < n_rem; ++i) {
-            const int ci = rc[i];
-            r += (ci > cj || (ci == cj && i < j)) ? 1 : 0;
-          }
-          if (r == my_rank) *res = item_begin + k_full * grid + j;
-        }
-      }
-      __syncthreads();
-      tail_item = *res;
-      __syncthreads();             // scratch free before the Q loads
-    } else if ((blockIdx.x + (long long)k_full * rot) % grid < n_rem) {
-      tail_item = item_begin + k_full * grid + (int)((blockIdx.x + (long long)k_full * rot) % grid);
-    }
-  }
-  const int n_mine = ORDER == 0 ? sm->hi - sm->lo : k_full + (tail_item >= 0 ? 1 : 0);
+  const int n_mine = ORDER == 0 ? sm->hi - sm->lo
+                                : k_full + (((blockIdx.x + (long long)k_full * rot) % grid) <
+                                                    N_items - k_full * grid ? 1 : 0);
   const int range_lo = ORDER == 0 ? sm->lo : 0;
   auto item_at = [&](int li) -> int {
     if (ORDER == 0) return range_lo + li;
-    if (li == k_full) return tail_item;
     return item_begin + li * grid + (int)((blockIdx.x + (long long)li * rot) % grid);
   };
   SV_STAMP_CTA(7600)
