@@ -79,9 +79,18 @@ constexpr int WARP_MMA = 8, WARP_KV = 9, WARP_Q = 10, WARP_ZERO = 11, WARP_EPI =
 // setmaxnreg moves registers inside the CTA's own pool (launch: 16 warps x 128): the 8 softmax
 // warps take 8 x 72 more, WG2 gives 4 x 64 and WG3 4 x 80 back.
 constexpr int REG_LAUNCH = 128;
-constexpr int REG_SOFTMAX = 200;
-constexpr int REG_PRODUCER = 64;         // WG2: MMA issuer, loaders
-constexpr int REG_EPILOGUE = 48;         // WG3
+#ifndef SV_REG_SOFTMAX
+#define SV_REG_SOFTMAX 200
+#endif
+#ifndef SV_REG_PRODUCER
+#define SV_REG_PRODUCER 64
+#endif
+#ifndef SV_REG_EPILOGUE
+#define SV_REG_EPILOGUE 48
+#endif
+constexpr int REG_SOFTMAX = SV_REG_SOFTMAX;
+constexpr int REG_PRODUCER = SV_REG_PRODUCER;   // WG2: MMA issuer, loaders
+constexpr int REG_EPILOGUE = SV_REG_EPILOGUE;   // WG3
 static_assert(8 * (REG_SOFTMAX - REG_LAUNCH) <=
                   4 * (REG_LAUNCH - REG_PRODUCER) + 4 * (REG_LAUNCH - REG_EPILOGUE),
               "register pool");
@@ -118,6 +127,9 @@ constexpr int ORDER = SV_ORDER;
 #ifndef SV_MMA_POLL
 #define SV_MMA_POLL 1
 #endif
+#ifndef SV_MMA_SHADOW
+#define SV_MMA_SHADOW 1
+#endif
 // The MMA issuer polls its barriers (mbarrier.test_wait) instead of try_wait, which may
 // suspend the thread: a suspended issuer wakes late and leaves the tensor pipe idle (-2.3% CSLA
 // time in shuffled-order timing; polling in the K/V loader or the softmax warps gains nothing).
@@ -148,6 +160,7 @@ struct Small {
   uint8_t meta[MAX_TILES];      // slot | buf << 1 | (use parity of buf) << 3, or EMPTY_TILE
   uint8_t eord[MAX_TILES];      // completion order (for the epilogue)
   int T, Tn, lo, hi, uses;
+  int mma_st[5];                // SV_MMA_SHADOW: issuer state between schedule batches
   uint32_t tmem_slot;
   uint64_t bars[2 * NQB + 2 * 8 + 14];
 };
@@ -338,6 +351,9 @@ attn_fwd_kernel(const __grid_constant__ CUtensorMap tmap_q,
       mbar_init(st_free + t, BM);
     }
     sm->uses = 0;
+#if SV_MMA_SHADOW
+    for (int i = 0; i < 5; ++i) sm->mma_st[i] = 0;
+#endif
     fence_barrier_init();
   }
   if (warp == WARP_KV && lane == 0) {
@@ -632,6 +648,17 @@ attn_fwd_kernel(const __grid_constant__ CUtensorMap tmap_q,
         // -------------------------------------------------------------- tcgen05 issuer
         // The whole warp runs the control flow so descriptors stay warp-uniform (uniform
         // registers); one elected lane issues each tcgen05 instruction.
+#if SV_MMA_SHADOW
+        // The persistent role state is live across every role's branch, so ptxas keeps it on
+        // the stack (the kernel is compiled at 128 registers; setmaxnreg does not change that)
+        // and the issuer paid an LDL/STL per op.  Shadow copies scoped to this branch stay in
+        // registers; they are written back once per schedule batch.
+        // (Plain shadow copies are folded away in SSA form: the state is kept in shared memory
+        // between batches instead, so it is not live across the other roles' branches at all.)
+        {
+        int kv_idx = sm->mma_st[0], tiles0 = sm->mma_st[1], tiles1 = sm->mma_st[2];
+        uint32_t p_cnt0 = (uint32_t)sm->mma_st[3], p_cnt1 = (uint32_t)sm->mma_st[4];
+#endif
         constexpr uint32_t IDESC_QK = idesc_bf16_f32(BM, BLK, 0, 0);
         constexpr uint32_t IDESC_PV = idesc_bf16_f32(BM, D, 0, 1);
         constexpr int KH = BLK >= 64 ? BLK / 32 : BLK / 16;  // P.V K-steps of the first P half
@@ -751,6 +778,15 @@ attn_fwd_kernel(const __grid_constant__ CUtensorMap tmap_q,
           }
         }
         if (lane == 0) SV_ACC(6800, SV_CLK() - tm0_)
+#if SV_MMA_SHADOW
+        __syncwarp();
+        if (lane == 0) {
+          sm->mma_st[0] = kv_idx; sm->mma_st[1] = tiles0; sm->mma_st[2] = tiles1;
+          sm->mma_st[3] = (int)p_cnt0; sm->mma_st[4] = (int)p_cnt1;
+        }
+        __syncwarp();
+        }
+#endif
       }
     } else {
       // ---------------------------------------------------------------- softmax warpgroups
