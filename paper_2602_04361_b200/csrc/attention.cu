@@ -130,6 +130,9 @@ constexpr int ORDER = SV_ORDER;
 #ifndef SV_MMA_SHADOW
 #define SV_MMA_SHADOW 1
 #endif
+#ifndef SV_SFX_SHADOW
+#define SV_SFX_SHADOW 1
+#endif
 // The MMA issuer polls its barriers (mbarrier.test_wait) instead of try_wait, which may
 // suspend the thread: a suspended issuer wakes late and leaves the tensor pipe idle (-2.3% CSLA
 // time in shuffled-order timing; polling in the K/V loader or the softmax warps gains nothing).
@@ -161,6 +164,7 @@ struct Small {
   uint8_t eord[MAX_TILES];      // completion order (for the epilogue)
   int T, Tn, lo, hi, uses;
   int mma_st[5];                // SV_MMA_SHADOW: issuer state between schedule batches
+  int sfx_st[2][2];             // SV_SFX_SHADOW: per-slot softmax (S phases, tiles done)
   uint32_t tmem_slot;
   uint64_t bars[2 * NQB + 2 * 8 + 14];
 };
@@ -353,6 +357,9 @@ attn_fwd_kernel(const __grid_constant__ CUtensorMap tmap_q,
     sm->uses = 0;
 #if SV_MMA_SHADOW
     for (int i = 0; i < 5; ++i) sm->mma_st[i] = 0;
+#endif
+#if SV_SFX_SHADOW
+    for (int i = 0; i < 4; ++i) (&sm->sfx_st[0][0])[i] = 0;
 #endif
     fence_barrier_init();
   }
@@ -792,6 +799,13 @@ attn_fwd_kernel(const __grid_constant__ CUtensorMap tmap_q,
       // ---------------------------------------------------------------- softmax warpgroups
       reg_alloc<REG_SOFTMAX>();
       const int t = warp >> 2;                 // slot
+#if SV_SFX_SHADOW
+      // as for the issuer: this warpgroup's loop-carried counters live in shared memory between
+      // batches (one copy per slot), not across the other roles' branches
+      {
+      uint32_t s_cnt = (uint32_t)sm->sfx_st[t][0];
+      int tiles0 = sm->sfx_st[t][1], tiles1 = sm->sfx_st[t][1];
+#endif
       const int quarter = warp & 3;
       const int row = quarter * 32 + lane;
       const uint32_t t_row = tmem + (uint32_t(quarter * 32) << 16);
@@ -966,6 +980,13 @@ attn_fwd_kernel(const __grid_constant__ CUtensorMap tmap_q,
                                         live ? (m * 0.69314718055994531f + logf(l)) : -INFINITY);
         mbar_arrive(st_bar + t);
       }
+#if SV_SFX_SHADOW
+      if ((threadIdx.x & 127) == 0) {        // read back only after the batch's __syncthreads
+        sm->sfx_st[t][0] = (int)s_cnt;
+        sm->sfx_st[t][1] = t ? tiles1 : tiles0;
+      }
+      }
+#endif
       reg_dealloc<REG_LAUNCH>();
     }
     __syncthreads();
