@@ -209,3 +209,34 @@ def test_persistent_schedule_mixed_lengths(sv, B):
                                 merge_lists([m[b]]), rows=live)
             sel = np.concatenate([np.arange(u * B, min((u + 1) * B, sched.N(K))) for u in live])
             _check(o[b], want, rows=sel)
+
+
+def test_persistent_schedule_several_batches(sv):
+    """More than MAX_TILES (96) tiles per CTA, so every CTA runs a second schedule batch: the
+    role state carried from one batch to the next (KV ring position, P and S phases, tiles done,
+    Q-buffer use parities) must continue exactly.  Small tiles (N_K = 1024, 8 query tiles per
+    head) with 1850 heads = 14800 tiles = 100 per CTA on 148 SMs; heads from the last window
+    (second batch) and the first are compared with the oracle."""
+    sides, K, B, D, bh = [1, 2, 4, 8, 16, 32], 6, 128, 128, 1850
+    sched = Schedule(sides)
+    q = q_iid(3, K, 0, bh, sched.N(K), D, device="cuda")
+    k, v = kv_cache_iid(3, 0, bh, sched.C(K), D, device="cuda")
+    gq, gkv = ceil_div(sched.N(K), B), ceil_div(sched.C(K), B)
+    rng = np.random.default_rng(5)
+    m = rng.random((bh, gq, gkv)) < 0.35
+    m[:, :, 0] = True                                    # sink block in every row
+    m[rng.random((bh, gq)) < 0.05] = False               # a few empty rows
+    rp, ci, st = _lists_from_bool(sv, m)
+    o = sv.block_sparse_attn(sides, K, B, q, k, v, rp, ci)
+    torch.cuda.synchronize()
+    assert st.item() in (0, 5)
+    for b in [0, 1, 900, bh - 60, bh - 2, bh - 1]:
+        live = [u for u in range(gq) if m[b, u].any()]
+        for u in range(gq):
+            if not m[b, u].any():
+                assert (o[b, u * B:(u + 1) * B] == 0).all()
+        if live:
+            want = block_sparse(to_np(q[b]), to_np(k[b]), to_np(v[b]), sched.C(K), B,
+                                merge_lists([m[b]]), rows=live)
+            sel = np.concatenate([np.arange(u * B, min((u + 1) * B, sched.N(K))) for u in live])
+            _check(o[b], want, rows=sel)
