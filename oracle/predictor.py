@@ -4,8 +4,15 @@ Definitions followed (§3.2 "Sparse Decision Scale", App. "Hardware-Eff
 Computation")
   P^(S) = Softmax(Q^(S) K^(S)T / sqrt(d))  over the keys j < C_S
   column sums D^(S)_{b,h,i,j} = sum_{q in query block i} P^(S)_{b,h,q,j}
-  Top-k over the column sums -> inds^(S)
-  inds <- A_sink U inds  (sinks added after the selection)
+  Top-k over the column sums -> inds^(S)  (the Top-K alone)
+  The paper adds the sink only at the target, after the mapping:
+        inds^(k) <- Concat(S, inds^(k))                                       PAPER.md:309-315
+        inds^(K) = A_sink U M_{S->K}(inds^(S))
+  READING 25: `sink_scales` of predict_pattern is therefore 0 on the paper-literal path (the
+      default composition, oracle/cs4a.py).  A positive value gives the alternative
+      "sink_in_source" composition — the sink OR-ed into the S-level pattern after the selection,
+      which the mapping then carries to K — kept as an option (north_star: "always including the
+      attention-sink blocks ... (2) carries that block pattern").
   READING 10: the predictor works at block granularity with the attention block size B, so the
       scored quantity is the block mass  mass[u, v] = sum_{j in KV block v, j < C_S} D[u, j]
       (= sum_{q in u} sum_{j in v} P[q, j]), and inds are KV *blocks*.
@@ -74,7 +81,8 @@ def predict_pattern(q: np.ndarray, k: np.ndarray, sched: Schedule, S: int, B: in
                     sink_scales: int, mode: str = "topk", topk: int = 1, tau: float = 0.0,
                     scale: Optional[float] = None):
     """Boolean source pattern (G_S x G_kvS) for one (b, h), plus the masses.
-    Selection first, then the sink union (PAPER.md:888 order)."""
+    Selection first; sink_scales > 0 then ORs the sink blocks into the S-level
+    pattern (READING 25's "sink_in_source" option; the paper adds them at the target only)."""
     mass = block_mass(q, k, sched, S, B, scale)
     gq, gkv = mass.shape
     n_q = sched.N(S)

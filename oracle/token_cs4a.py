@@ -8,7 +8,8 @@ Definitions followed
   Column-Sum  A^(S)[g, j] = sum_{q in block g} P^(S)[q, j]
   inds^(S)[g] = TopK_j A^(S)[g, :] with k = ceil(alpha C_S) keys
         (READING 11: "Top-K around 0.2" is the fraction alpha of the keys; ties go
-        to the smaller j), then the sink tokens j < C_sink are added
+        to the smaller j).  The paper adds no sink at S; select_tokens'
+        n_sink_tokens > 0 is READING 25's "sink_in_source" option, 0 on the paper-literal path
   M_{S->K}: target query block g_K reads source block phi(g_K)
         (oracle/mapping.phi with C-row blocks); each selected source token is projected by
         Decompose-Align-Project with the forward-interval footprint
@@ -49,7 +50,8 @@ def colsum(q: np.ndarray, k: np.ndarray, n_kv: int, C: int) -> np.ndarray:
 
 
 def select_tokens(a_row: np.ndarray, k_tok: int, n_sink_tokens: int) -> np.ndarray:
-    """TopK of one column-sum row (ties to the smaller j), then the sink tokens."""
+    """TopK of one column-sum row (ties to the smaller j), then the first n_sink_tokens tokens
+    (0 in the paper-literal order, READING 25)."""
     order = sorted(range(len(a_row)), key=lambda j: (-a_row[j], j))
     sel = np.zeros(len(a_row), dtype=bool)
     sel[order[:k_tok]] = True
