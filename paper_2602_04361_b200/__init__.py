@@ -484,6 +484,11 @@ class SparseLayer:
                      -> block_sparse_attn
         union      : all three masks OR-ed (READING 19)
 
+    Sink order (DESIGN.md READING 25): by default the S-level pattern is the Top-K alone
+     and the sink is added by the mapping at K (A_sink U M(inds^(S)),
+    PAPER.md:883-890).  sink_in_source=True ORs the sink into the S-level pattern as well, so
+    the mapping also carries the sink blocks' footprint to K.
+
     Buffers for masks and lists are allocated once (sized from the geometry) and reused, so a
     step is kernel launches only.
     """
@@ -491,9 +496,11 @@ class SparseLayer:
     def __init__(self, sides, target: int, decision: int, block: int, bh: int,
                  sink_scales: int = 5, windows=(7, 5, 3, 1, 1), select_mode=SELECT_TOPK,
                  topk: int = 5, threshold: float = 0.01, map_mode=MAP_FOOTPRINT,
-                 kinds: Sequence[str] = ("csla", "cs4a", "union")):
+                 kinds: Sequence[str] = ("csla", "cs4a", "union"), sink_in_source: bool = False):
         self.sides, self.K, self.S, self.B, self.bh = list(sides), target, decision, block, bh
         self.sink, self.windows = sink_scales, tuple(windows)
+        self.sink_in_source = bool(sink_in_source)
+        self.sink_S = sink_scales if sink_in_source else 0      # READING 25
         self.kinds = tuple(kinds)   # list sets built by build_patterns (READING 19 policies)
         self.select_mode, self.topk, self.threshold, self.map_mode = select_mode, topk, threshold, map_mode
         gk, gs = geometry(sides, target, block), geometry(sides, decision, block)
@@ -514,7 +521,7 @@ class SparseLayer:
     def build_patterns(self, q_S, k_cache, stream=None):
         """a1-a5: CSLA mask, decision-scale prediction, mapping, and the three CSR list sets."""
         local_mask(self.sides, self.K, self.B, self.sink, self.windows, out=self.local, stream=stream)
-        predict_pattern(self.sides, self.S, self.B, self.sink, q_S, k_cache, self.select_mode,
+        predict_pattern(self.sides, self.S, self.B, self.sink_S, q_S, k_cache, self.select_mode,
                         self.topk, self.threshold, mask_out=self.src, mass_out=self.mass,
                         stream=stream)
         map_indices(self.sides, self.S, self.K, self.B, self.sink, self.src, self.map_mode,

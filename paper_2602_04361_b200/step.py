@@ -4,6 +4,8 @@ across all layers, as the paper deploys SparVAR.
 Per layer, at the decision scale S the model runs full attention; the target
 scales S+1..K run block-sparse attention:
 
+  Sink order (DESIGN.md READING 25): the S-level pattern is the Top-K alone and the map adds the
+  sink at each target; sink_in_source=True ORs it in at S as well.
   CS4A layers (the first round(0.6 L), "substituted from the shallowest"):
       O_S, pattern = dense attention at S with the block masses read off its softmax and
                      selected (top-k / threshold)                (sparvar_dense_attn_mass;
@@ -57,13 +59,14 @@ class SparsifiedStep:
                  sink_scales: int = 5, windows=(7, 5, 3, 1, 1), select_mode=SELECT_TOPK,
                  topk: int = 5, threshold: float = 0.01, map_mode=MAP_FOOTPRINT,
                  fused: bool = True, granularity: str = "block", query_block: int = 192,
-                 alpha: float = 0.2):
+                 alpha: float = 0.2, sink_in_source: bool = False):
         if not 1 <= decision < target <= len(sides):
             raise ValueError("need 1 <= decision < target <= number of scales")
         self.sides, self.S, self.K, self.B, self.bh = list(sides), decision, target, block, bh
         self.layers, self.D = layers, head_dim
         self.n_cs4a = layer_split(layers, cs4a_fraction)
         self.sink, self.windows = sink_scales, tuple(windows)
+        self.sink_S = sink_scales if sink_in_source else 0          # READING 25
         self.select_mode, self.topk, self.threshold, self.map_mode = select_mode, topk, threshold, map_mode
         self.targets = list(range(decision + 1, target + 1))
         dev = "cuda"
@@ -116,7 +119,7 @@ class SparsifiedStep:
         S, C = self.S, self.C
         dense_attn(self.sides, S, q[S], k_cache, v_cache, o=out[S], lse=self.lse, stream=stream)
         token_colsum(self.sides, S, C, q[S], k_cache, self.lse, out=self.colsum, stream=stream)
-        token_select(self.sides, S, C, self.sink, self.colsum, self.k_tok, out=self.tsel,
+        token_select(self.sides, S, C, self.sink_S, self.colsum, self.k_tok, out=self.tsel,
                      stream=stream)
         rpS, ciS, capS, G_S, nS = self.tlists_S
         build_block_lists(self.bh, G_S, nS, [(self.tsel, False)], capS, rpS, ciS, self.status,
@@ -158,13 +161,13 @@ class SparsifiedStep:
         elif self.kind(l) == "cs4a":
             gS = self.gS
             if self.fused:
-                dense_attn_mass(self.sides, S, B, self.sink, q[S], k_cache, v_cache,
+                dense_attn_mass(self.sides, S, B, self.sink_S, q[S], k_cache, v_cache,
                                 self.select_mode, self.topk, self.threshold, o=out[S],
                                 want_mass=False, mask_out=self.src, workspace=self.ws,
                                 stream=stream)
             else:
                 dense_attn(self.sides, S, q[S], k_cache, v_cache, o=out[S], stream=stream)
-                predict_pattern(self.sides, S, B, self.sink, q[S], k_cache, self.select_mode,
+                predict_pattern(self.sides, S, B, self.sink_S, q[S], k_cache, self.select_mode,
                                 self.topk, self.threshold, want_mass=False, mask_out=self.src,
                                 stream=stream)
             rpS, ciS, capS = self.lists_S

@@ -51,10 +51,10 @@ def test_bench_workload_sampled_units():
         for u in range(gS_q):
             sel = np.zeros(gS_kv, dtype=bool)
             sel[select_topk(mass[b, u].astype(np.float32).astype(np.float64), topk)] = True
-            sel[:nsb] = True
-            assert np.array_equal(sel, src[b, u]), (b, u)
+            assert np.array_equal(sel, src[b, u]), (b, u)      # Top-K only at S (READING 25)
         # mapping and lists
         assert np.array_equal(mapped[b], map_pattern(src[b], sched, S, K, B, sink, "footprint"))
+        assert mapped[b][:, :nsb].all()                        # A_sink U M(inds^(S))
         for u in range(gK_q):
             assert np.array_equal(csla_lists[b * gK_q + u], np.nonzero(local[u])[0])
             assert np.array_equal(cs4a_lists[b * gK_q + u], np.nonzero(mapped[b, u])[0])
