@@ -1,20 +1,33 @@
 """bench.py — SparVAR hot path on B200: last-scale block-sparse attention ms/layer.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference] [--config 8b|2b]
+                    [--scaling strong|weak] [--dry-run]
     python -m torch.distributed.run --nnodes=1 --nproc-per-node N --master-addr 127.0.0.1 \
         --master-port P bench.py --gpus N ...
 
-Workload (N=1): Infinity-8B-shaped last scale (BASELINE.json configs[3]): schedule 1..64
-(13 scales, q 4096 x kv 10521), decision scale S=11, block 128, head_dim 128, batch 4 x 24 heads
-= 96 (b,h) units, bf16.  N>1: weak scaling, every rank runs its own 96 units (global batch 4N,
-(batch x head) sharding, no data-path collective).
+`--gpus N` without a torchrun environment re-launches itself under torch.distributed.run with N
+ranks (one per GPU); under torchrun WORLD_SIZE must equal --gpus.
 
-One step = one pass of the whole hot path (DESIGN.md "Path"):
+Workload: BASELINE.json configs[3], the Infinity-8B-shaped last scale: schedule 1..64 (13 scales,
+q 4096 x kv 10521), decision scale S = 11, block 128, head_dim 128, batch 4 x 24 heads = 96 (b,h)
+units, bf16.  Default `--scaling strong`: the 96 units are split over the N
+ranks, rank r takes [r*96/N, (r+1)*96/N) (96 / 48 / 24 / 12 per GPU at N = 1/2/4/8), each rank
+regenerates its own inputs from the counter-based generator keyed by the GLOBAL unit index, and
+there is no collective on the data path.  `--scaling weak` runs 96 units on every rank (global
+batch 4N) and says so in config.workload.
+
+One step = one pass of the whole hot path (DESIGN.md §1):
     a1 local_mask(13) | a2+a3 predict_pattern(S=11, top-5) | a4 map_indices(11->13)
     a5 build_block_lists for the CSLA layer (sink+local) and the CS4A layer (sink+mapped)
     a6 block_sparse_attn for the CSLA layer and for the CS4A layer
-`value` = ms per layer = step time / 2 (two attention layers per step, pattern work included).
-The dense sm_100a kernel on the same shape (a7) is timed separately for the speed-up.
+The CS4A pattern uses the paper's sink order (READING 25): Top-K only at S, A_sink U M(TopK) at K.
+`value` = ms per layer = job step time (max over ranks) / 2.  The dense sm_100a kernel on the
+same shape (a7) is timed separately for the speed-up.
+
+After timing (untimed): every rank's full output shards (both layers) and its pattern tensors
+are all-gathered to rank 0 (all_gather_into_tensor over NCCL), and rank 0 checks sampled query
+blocks of units owned by EVERY rank against the fp64 oracle (`oracle_check`, the bench's oracle
+leg together with `cpu_baseline` / `--impl reference`).
 """
 from __future__ import annotations
 
@@ -22,6 +35,7 @@ import argparse
 import json
 import math
 import os
+import socket
 import statistics
 import subprocess
 import sys
@@ -37,18 +51,153 @@ CONFIGS = {
     "8b": dict(name="infinity8b_last_scale", batch=4, heads=24),
     "2b": dict(name="infinity2b_last_scale", batch=1, heads=16),
 }
-K_T, S_D, BLOCK, D, SINK, WINDOWS, TOPK = 13, 11, 128, 128, 5, (7, 5, 3, 1, 1), 5
+# the geometry of the hot path
+GEOM = dict(sides=SIDES, K=13, S=11, B=128, D=128, sink=5, windows=(7, 5, 3, 1, 1), topk=5)
+LAUNCHES_PER_STEP = 7   # local_mask, predictor, map, 2x build_lists, 2x attention
 
 
-def parse():
+def parse(argv=None):
     p = argparse.ArgumentParser()
     p.add_argument("--gpus", type=int, default=1)
     p.add_argument("--steps", type=int, default=50)
     p.add_argument("--warmup", type=int, default=5)
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
     p.add_argument("--config", default="8b", choices=list(CONFIGS))
+    p.add_argument("--scaling", default="strong", choices=["strong", "weak"])
     p.add_argument("--no-cpu-baseline", action="store_true")
-    return p.parse_args()
+    p.add_argument("--dry-run", action="store_true",
+                   help="print the per-rank unit ranges for --gpus and exit")
+    return p.parse_args(argv)
+
+
+# ----------------------------------------------------------------------------- orchestration
+def unit_ranges(world: int, units: int, scaling: str):
+    """Global (b,h) unit range of every rank: strong = `units` split contiguously (SURVEY.md
+    §8(e)), weak = `units` per rank."""
+    from paper_2602_04361_b200.shard import strong_units_ranges, weak_units
+    if scaling == "strong":
+        return strong_units_ranges(world, units)
+    return [weak_units(r, units) for r in range(world)]
+
+
+def free_port() -> int:
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def maybe_spawn(args) -> int | None:
+    """`--gpus N` outside torchrun: re-run this file under torch.distributed.run with N ranks.
+    Returns the child's exit code, or None when this process is already a rank."""
+    if "WORLD_SIZE" in os.environ:
+        world = int(os.environ["WORLD_SIZE"])
+        if world != args.gpus:
+            raise SystemExit(f"bench.py: WORLD_SIZE={world} but --gpus {args.gpus}")
+        return None
+    if args.gpus <= 1:
+        return None
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr", "127.0.0.1",
+           "--master-port", str(free_port()), os.path.abspath(__file__), *sys.argv[1:]]
+    return subprocess.call(cmd)
+
+
+def gather_shards(tensors: dict, n_max: int):
+    """All-gather every rank's shard tensors (first dim = its units, padded to n_max) to rank 0:
+    name -> (world, n_max, ...) on rank 0, None elsewhere.  all_gather_into_tensor over NCCL on
+    the GPU box; gloo (list all_gather) in the CPU tests."""
+    import torch
+    import torch.distributed as dist
+    out = {}
+    dist_on = dist.is_available() and dist.is_initialized() and dist.get_world_size() > 1
+    for name, t in tensors.items():
+        pad = torch.zeros((n_max,) + tuple(t.shape[1:]), dtype=t.dtype, device=t.device)
+        pad[:t.shape[0]] = t
+        if not dist_on:
+            out[name] = pad.unsqueeze(0)
+            continue
+        world = dist.get_world_size()
+        if dist.get_backend() == "nccl":
+            g = torch.empty((world,) + tuple(pad.shape), dtype=pad.dtype, device=pad.device)
+            dist.all_gather_into_tensor(g, pad.contiguous())
+        else:
+            parts = [torch.empty_like(pad) for _ in range(world)]
+            dist.all_gather(parts, pad.contiguous())
+            g = torch.stack(parts)
+        out[name] = g
+    if dist_on and dist.get_rank() != 0:
+        return None
+    return out
+
+
+def sample_blocks(g_q: int):
+    return sorted({0, g_q // 2, g_q - 1})
+
+
+def oracle_check(geom: dict, ranges, gathered: dict, seed: int = 0, units_per_rank: int = 1):
+    """Rank 0: compare sampled outputs of units owned by every rank with the fp64 oracle.
+
+    For each sampled unit: the CSLA output rows of sampled query blocks against the oracle's
+    block-sparse attention over the CSLA lists; the S-level selection against the oracle's Top-K
+    rule on the GPU's own fp32 masses (protocol (i), bit-exact); the mapped pattern against
+    the oracle's map of that selection plus the sink (READING 25, bit-exact); the CS4A output
+    rows against the oracle's attention over that pattern.  Attention within the north-star
+    bound (max|d| <= 1e-2, mean|d| <= 1e-3)."""
+    import numpy as np
+    from oracle.attention import block_sparse, merge_lists
+    from oracle.csla import local_block_mask
+    from oracle.geometry import Schedule, ceil_div
+    from oracle.mapping import map_pattern
+    from oracle.predictor import select_topk
+    from synth import kv_cache_iid, q_iid
+
+    sides, K, S, B, D = geom["sides"], geom["K"], geom["S"], geom["B"], geom["D"]
+    sched = Schedule(sides)
+    n_q, n_kv = sched.N(K), sched.C(K)
+    gK_q, gK_kv = ceil_div(n_q, B), ceil_div(n_kv, B)
+    gS_q, gS_kv = ceil_div(sched.N(S), B), ceil_div(sched.C(S), B)
+    local = local_block_mask(sched, K, B, geom["sink"], geom["windows"])
+    lists_csla = merge_lists([local])
+    blocks = sample_blocks(gK_q)
+    rows = np.concatenate([np.arange(u * B, min((u + 1) * B, n_q)) for u in blocks])
+
+    def bits(words, n):
+        w = np.asarray(words, dtype=np.int64) & 0xFFFFFFFF
+        b = (w[..., :, None] >> np.arange(32)) & 1
+        return b.reshape(*w.shape[:-1], -1)[..., :n].astype(bool)
+
+    res = {"units_checked": [], "max_abs": 0.0, "mean_abs": 0.0, "patterns_exact": True}
+    ok = True
+    for r, (a, b) in enumerate(ranges):
+        picks = list(range(a, min(b, a + units_per_rank)))
+        if r == len(ranges) - 1 and b - 1 not in picks:
+            picks.append(b - 1)
+        for unit in picks:
+            i = unit - a
+            q = q_iid(seed, K, unit, 1, n_q, D)[0].double().numpy()
+            k, v = kv_cache_iid(seed, unit, 1, n_kv, D)
+            k, v = k[0].double().numpy(), v[0].double().numpy()
+            mass = gathered["mass"][r, i].double().cpu().numpy()
+            src = bits(gathered["src"][r, i].cpu().numpy(), gS_kv)
+            mapped = bits(gathered["mapped"][r, i].cpu().numpy(), gK_kv)
+            for u in range(gS_q):
+                want = np.zeros(gS_kv, dtype=bool)
+                want[select_topk(mass[u].astype(np.float32).astype(np.float64), geom["topk"])] = True
+                if not np.array_equal(want, src[u]):
+                    res["patterns_exact"] = ok = False
+            want_map = map_pattern(src, sched, S, K, B, geom["sink"], "footprint")
+            if not np.array_equal(want_map, mapped):
+                res["patterns_exact"] = ok = False
+            for name, lists in (("o_csla", lists_csla), ("o_cs4a", merge_lists([want_map]))):
+                want_o = block_sparse(q, k, v, n_kv, B, lists, rows=blocks)
+                got = gathered[name][r, i].double().cpu().numpy()
+                d = np.abs(got[rows] - want_o[rows])
+                res["max_abs"] = max(res["max_abs"], float(d.max()))
+                res["mean_abs"] = max(res["mean_abs"], float(d.mean()))
+            res["units_checked"].append(unit)
+    res["ok"] = bool(ok and res["max_abs"] <= 1e-2 and res["mean_abs"] <= 1e-3)
+    res["query_blocks"] = blocks
+    return res
 
 
 # ----------------------------------------------------------------------------- clocks
@@ -64,7 +213,7 @@ class ClockSampler:
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
-                 "--format=csv,noheader,nounits", "-lms", "100"],
+                 "--format=csv,noheader,nounits", "-lms", "50"],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.th = threading.Thread(target=self._read, daemon=True)
             self.th.start()
@@ -99,7 +248,19 @@ def peaks():
     try:
         return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))), "measured"
     except Exception:
+        # /opt/skills/guides/B200_PROFILING.md fallback figures
         return {"bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0, "hbm_gbs": 6650.0}, "fallback"
+
+
+def pick_peak(pk: dict, timed_s: float, clk: dict):
+    """Burst peak for a short timed region or clocks at max; sustained otherwise (the measured
+    sustained cuBLAS figure is taken after seconds of load at a power-capped clock)."""
+    sm, mx = clk.get("sm_mhz"), clk.get("sm_max_mhz")
+    at_max = sm is not None and mx and sm >= 0.95 * mx
+    if timed_s < 1.0 or at_max:
+        return float(pk.get("bf16_tflops", 1590.0)), "bf16_tflops (burst): timed region %.3f s%s" % (
+            timed_s, ", clocks at max" if at_max else "")
+    return float(pk.get("bf16_tflops_sustained", 1400.0)), "bf16_tflops_sustained: timed region %.1f s" % timed_s
 
 
 def algorithmic_flops(lists, n_q, n_kv, B, Dh):
@@ -112,85 +273,103 @@ def algorithmic_flops(lists, n_q, n_kv, B, Dh):
     return 4 * Dh * tot
 
 
-def traffic_from_profile(kernel="attn_fwd_kernel"):
+def profile_numbers():
     p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     try:
-        d = json.load(open(p))
-        return d.get(kernel)
+        return json.load(open(p))
+    except Exception:
+        return {}
+
+
+def cpu_cores() -> int:
+    return len(os.sched_getaffinity(0))
+
+
+# ----------------------------------------------------------------------------- CPU oracle timing
+def oracle_units(seed, units, geom, budget_s=15.0, max_units=4, dense=True):
+    """Time the fp64 oracle (BLAS threads = the host cores this process may use) on a bounded
+    sample of the workload's units: the CSLA mask once (shared by all heads), then per unit the
+    predictor (O4), the map (O5), the list merge and both block-sparse attentions (O7), and the
+    dense attention (O8) of the same unit.  Returns per-unit seconds."""
+    import numpy as np
+    from oracle.attention import block_sparse, dense as dense_attn, merge_lists
+    from oracle.cs4a import cs4a_patterns
+    from oracle.csla import local_block_mask
+    from oracle.geometry import Schedule
+    from synth import kv_cache_iid, q_iid
+
+    sides, K, S, B, D = geom["sides"], geom["K"], geom["S"], geom["B"], geom["D"]
+    sched = Schedule(sides)
+    t0 = time.perf_counter()
+    local = local_block_mask(sched, K, B, geom["sink"], geom["windows"])
+    t_mask = time.perf_counter() - t0
+    t_sparse, t_dense, n = 0.0, 0.0, 0
+    while n < min(max_units, len(units)) and (n == 0 or t_mask + t_sparse + t_dense < budget_s):
+        u = units[n]
+        q = q_iid(seed, K, u, 1, sched.N(K), D)[0].double().numpy()
+        qs = q_iid(seed, S, u, 1, sched.N(S), D)[0].double().numpy()
+        k, v = kv_cache_iid(seed, u, 1, sched.C(K), D)
+        k, v = k[0].double().numpy(), v[0].double().numpy()
+        t1 = time.perf_counter()
+        _, mapped, _ = cs4a_patterns(qs, k, sched, S, K, B, geom["sink"], "topk", geom["topk"])
+        block_sparse(q, k, v, sched.C(K), B, merge_lists([local]))
+        block_sparse(q, k, v, sched.C(K), B, merge_lists([mapped]))
+        t2 = time.perf_counter()
+        if dense:
+            dense_attn(q, k, v, sched.C(K))
+        t3 = time.perf_counter()
+        t_sparse += t2 - t1
+        t_dense += t3 - t2
+        n += 1
+    return {"t_mask": t_mask, "t_sparse_unit": t_sparse / n, "t_dense_unit": t_dense / n, "n": n}
+
+
+def _limit_blas(cores):
+    try:
+        from threadpoolctl import threadpool_limits
+        return threadpool_limits(cores)
     except Exception:
         return None
 
 
-# ----------------------------------------------------------------------------- CPU oracle
-def oracle_sample(seed, bh_global, budget_s=12.0, max_heads=8):
-    """Time the fp64 oracle on a bounded sample of the workload: the CSLA mask (shared by all
-    heads) plus predictor, mapping, list merge and both block-sparse attentions for as many (b,h)
-    units as fit in ~budget_s.  Returns (ms per layer extrapolated to all units, sample text)."""
-    import numpy as np
-    from oracle.attention import block_sparse, merge_lists
-    from oracle.csla import local_block_mask
-    from oracle.geometry import Schedule
-    from oracle.mapping import map_pattern
-    from oracle.predictor import predict_pattern
-    from synth import kv_cache_iid, q_iid
-
-    sched = Schedule(SIDES)
-    t0 = time.perf_counter()
-    local = local_block_mask(sched, K_T, BLOCK, SINK, WINDOWS)
-    t_mask = time.perf_counter() - t0
-    per_head, n = 0.0, 0
-    while n < max_heads and (n == 0 or (t_mask + per_head) < budget_s):
-        b = bh_global + n
-        q = q_iid(seed, K_T, b, 1, sched.N(K_T), D)[0].double().numpy()
-        qs = q_iid(seed, S_D, b, 1, sched.N(S_D), D)[0].double().numpy()
-        k, v = kv_cache_iid(seed, b, 1, sched.C(K_T), D)
-        k, v = k[0].double().numpy(), v[0].double().numpy()
-        t1 = time.perf_counter()
-        src, _ = predict_pattern(qs, k, sched, S_D, BLOCK, SINK, "topk", TOPK)
-        mapped = map_pattern(src, sched, S_D, K_T, BLOCK, SINK, "footprint")
-        block_sparse(q, k, v, sched.C(K_T), BLOCK, merge_lists([local]))
-        block_sparse(q, k, v, sched.C(K_T), BLOCK, merge_lists([mapped]))
-        per_head += time.perf_counter() - t1
-        n += 1
-    return t_mask, per_head / n, n
-
-
-def cpu_cores():
-    try:
-        from threadpoolctl import threadpool_info
-        info = [x for x in threadpool_info() if x.get("user_api") == "blas"]
-        if info:
-            return int(info[0]["num_threads"])
-    except Exception:
-        pass
-    return len(os.sched_getaffinity(0))
-
-
 # ----------------------------------------------------------------------------- reference arm
 def run_reference(args, rank, world):
+    """The oracle as it stands on the host cores (rank 0 only), each step a bounded sample of the
+    workload (one (b,h) unit of the 96 plus the shared CSLA mask), extrapolated linearly to all
+    units (the units are independent)."""
     cfg = CONFIGS[args.config]
     units = cfg["batch"] * cfg["heads"]
     if rank != 0:
         return 0
-    times = []
+    cores = cpu_cores()
+    _limit_blas(cores)
+    t_start = time.perf_counter()
+    times, sample_s = [], []
     for i in range(args.warmup + args.steps):
         t0 = time.perf_counter()
-        t_mask, t_head, n = oracle_sample(0, (i * 7) % units, budget_s=2.0, max_heads=1)
-        est_ms = (t_mask + units * t_head) * 1e3 / 2.0
+        r = oracle_units(0, [(i * 7) % units], GEOM, budget_s=0.0, max_units=1, dense=False)
+        dt = time.perf_counter() - t0
+        est_ms = (r["t_mask"] + units * r["t_sparse_unit"]) * 1e3 / 2.0
         if i >= args.warmup:
             times.append(est_ms)
+            sample_s.append(dt)
+    wall = time.perf_counter() - t_start
     v = statistics.median(times)
     line = {
         "impl": "reference", "metric": METRIC, "value": round(v, 3), "unit": "ms/layer",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": round(2 * v, 3), "higher_is_better": False, "scaling": "weak",
+        "ms_per_step": round(2 * v, 3), "higher_is_better": False, "scaling": args.scaling,
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": cfg["name"], "units_bh": units, "target_scale": K_T,
-                   "decision_scale": S_D, "block": BLOCK, "head_dim": D, "layers_per_step": 2},
-        "cpu_baseline": {"value": round(v, 3), "unit": "ms/layer", "cores": cpu_cores(),
+        "config": {"workload": cfg["name"], "units_bh": units, "target_scale": GEOM["K"],
+                   "decision_scale": GEOM["S"], "block": GEOM["B"], "head_dim": GEOM["D"],
+                   "layers_per_step": 2, "sample_fraction": f"1/{units} units per step"},
+        "cpu_baseline": {"value": round(v, 3), "unit": "ms/layer", "cores": cores,
                          "kind": "oracle",
-                         "sample": "per step: CSLA mask once + predictor/map/merge/2 attentions for "
-                                   "1 of %d (b,h) units, extrapolated to all units" % units},
+                         "sample": "per step: CSLA mask + predictor/map/merge/2 attentions for 1 of "
+                                   "%d (b,h) units (fp64 numpy, BLAS on %d threads), extrapolated "
+                                   "linearly to all units" % (units, cores)},
+        "measured": {"sample_s_per_step_median": round(statistics.median(sample_s), 3),
+                     "wall_s_total": round(wall, 2), "extrapolation_factor": units},
         "e2e": {"value": round(v, 3), "unit": "ms/layer", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
@@ -199,15 +378,25 @@ def run_reference(args, rank, world):
 
 
 # ----------------------------------------------------------------------------- our arm
-def main():
-    args = parse()
+def main(argv=None):
+    args = parse(argv)
+    cfg = CONFIGS[args.config]
+    units = cfg["batch"] * cfg["heads"]
+    if args.dry_run:
+        sys.path.insert(0, ROOT)
+        rr = unit_ranges(args.gpus, units, args.scaling)
+        for r, (a, b) in enumerate(rr):
+            print(f"rank {r}: units [{a},{b})")
+        return 0
+    rc = maybe_spawn(args)
+    if rc is not None:
+        return rc
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
     if args.impl == "reference":
         return run_reference(args, rank, world)
 
-    import numpy as np
     import torch
     import torch.distributed as dist
 
@@ -218,35 +407,46 @@ def main():
     from paper_2602_04361_b200 import shard as sv_shard
     from synth import kv_cache_iid, q_iid
 
-    cfg = CONFIGS[args.config]
-    units = cfg["batch"] * cfg["heads"]
-    bh0, _ = sv_shard.weak_units(rank, units)
+    G = GEOM
+    K_T, S_D, BLOCK, D = G["K"], G["S"], G["B"], G["D"]
+    ranges = unit_ranges(world, units, args.scaling)
+    bh0, bh1 = ranges[rank]
+    n_loc = bh1 - bh0
+    n_max = max(b - a for a, b in ranges)
     n_q, n_qS = SIDES[K_T - 1] ** 2, SIDES[S_D - 1] ** 2
     n_kv = sum(s * s for s in SIDES[:K_T])
     dev = torch.device("cuda", local_rank)
-    q = q_iid(0, K_T, bh0, units, n_q, D, device=dev)
-    qS = q_iid(0, S_D, bh0, units, n_qS, D, device=dev)
-    k, v = kv_cache_iid(0, bh0, units, n_kv, D, device=dev)
-    layer = sv.SparseLayer(SIDES, K_T, S_D, BLOCK, units, sink_scales=SINK, windows=WINDOWS, kinds=("csla", "cs4a"),
-                           topk=TOPK)
+    q = q_iid(0, K_T, bh0, n_loc, n_q, D, device=dev)
+    qS = q_iid(0, S_D, bh0, n_loc, n_qS, D, device=dev)
+    k, v = kv_cache_iid(0, bh0, n_loc, n_kv, D, device=dev)
+    layer = sv.SparseLayer(SIDES, K_T, S_D, BLOCK, n_loc, sink_scales=G["sink"],
+                           windows=G["windows"], kinds=("csla", "cs4a"), topk=G["topk"])
     o_csla = torch.empty_like(q)
     o_cs4a = torch.empty_like(q)
     stream = torch.cuda.current_stream()
-    ev_attn = []     # (start, end) events around every CSLA attention launch in the timed region
+    ev_attn, ev_pred = [], []     # (start, end) events around the CSLA attention / predictor
+
+    def ev():
+        return torch.cuda.Event(enable_timing=True)
 
     def step(record=False):
-        layer.build_patterns(qS, k)
         if record:
-            e0 = torch.cuda.Event(enable_timing=True)
-            e1 = torch.cuda.Event(enable_timing=True)
+            p0, p1 = ev(), ev()
+            p0.record(stream)
+            layer.predict(qS, k, stream=stream)
+            p1.record(stream)
+            ev_pred.append((p0, p1))
+            layer.build_patterns(qS, k, predict=False)
+            e0, e1 = ev(), ev()
             e0.record(stream)
-        layer.attend("csla", q, k, v, o=o_csla)
-        if record:
+            layer.attend("csla", q, k, v, o=o_csla)
             e1.record(stream)
             ev_attn.append((e0, e1))
+        else:
+            layer.build_patterns(qS, k)
+            layer.attend("csla", q, k, v, o=o_csla)
         layer.attend("cs4a", q, k, v, o=o_cs4a)
 
-    LAUNCHES_PER_STEP = 7   # local_mask, predictor, map, 2x build_lists, 2x attention
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
@@ -254,11 +454,11 @@ def main():
 
     clocks = ClockSampler(local_rank)
     clocks.start()
+    time.sleep(0.15)
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
-    t0 = torch.cuda.Event(enable_timing=True)
-    t1 = torch.cuda.Event(enable_timing=True)
+    t0, t1 = ev(), ev()
     t0.record(stream)
     for _ in range(args.steps):
         step(record=True)
@@ -269,20 +469,23 @@ def main():
     clk = clocks.stop()
     ms_step = t0.elapsed_time(t1) / args.steps
     attn_ms = statistics.mean(a.elapsed_time(b) for a, b in ev_attn)
-    ms_step, attn_ms = sv_shard.max_over_ranks([ms_step, attn_ms], device=dev)
+    pred_ms = statistics.mean(a.elapsed_time(b) for a, b in ev_pred)
+    ms_step, attn_ms_max, pred_ms_max = sv_shard.max_over_ranks([ms_step, attn_ms, pred_ms],
+                                                                device=dev)
 
     # --- dense denominator (a7), same shape, separately timed
     for _ in range(2):
         sv.dense_attn(SIDES, K_T, q, k, v, o=o_cs4a)
     torch.cuda.synchronize()
-    d0, d1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    d0, d1 = ev(), ev()
     nd = max(3, args.steps // 4)
     d0.record(stream)
     for _ in range(nd):
         sv.dense_attn(SIDES, K_T, q, k, v, o=o_cs4a)
     d1.record(stream)
     torch.cuda.synchronize()
-    dense_ms = d0.elapsed_time(d1) / nd
+    (dense_ms,) = sv_shard.max_over_ranks([d0.elapsed_time(d1) / nd], device=dev)
+    layer.attend("cs4a", q, k, v, o=o_cs4a)          # restore the CS4A output for validation
 
     # --- end to end through the public API with host buffers (pinned), copies timed.
     # Steps are pipelined the way a serving loop would run them: step i's inputs are copied in on
@@ -328,7 +531,7 @@ def main():
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0, e1 = ev(), ev()
     s_in.wait_stream(stream)
     e0.record(s_in)
     e2e_steps(ne)
@@ -336,99 +539,112 @@ def main():
     stream.wait_stream(s_in)
     e1.record(stream)
     torch.cuda.synchronize()
-    e2e_step = e0.elapsed_time(e1) / ne
-    (e2e_step,) = sv_shard.max_over_ranks([e2e_step], device=dev)
-    h2d = sum(x.numel() * x.element_size() for x in (hq, hqS, hk, hv))
-    d2h = 2 * hq.numel() * hq.element_size()
+    (e2e_step,) = sv_shard.max_over_ranks([e0.elapsed_time(e1) / ne], device=dev)
+    h2d = sum(x.numel() * x.element_size() for x in (hq, hqS, hk, hv)) * world
+    d2h = 2 * hq.numel() * hq.element_size() * world
+    del sets, hq, hqS, hk, hv, ho1, ho2
 
-    # --- FLOP accounting for the CSLA kernel (lists copied once, outside timing)
+    # --- pattern statistics + FLOP accounting (untimed)
+    layer.build_patterns(qS, k)
+    layer.attend("csla", q, k, v, o=o_csla)
+    layer.attend("cs4a", q, k, v, o=o_cs4a)
+    torch.cuda.synchronize()
     rp, ci = layer.lists["csla"]
     rp_h, ci_h = rp.cpu().numpy(), ci.cpu().numpy()
     g_q = layer.gk["G_q"]
     lists0 = [ci_h[rp_h[u]:rp_h[u + 1]] for u in range(g_q)]
-    alg_flops = algorithmic_flops(lists0, n_q, n_kv, BLOCK, D) * units   # mask shared by heads
+    alg_flops = algorithmic_flops(lists0, n_q, n_kv, BLOCK, D) * n_loc   # mask shared by heads
     nnz = int(rp_h[-1])
     exec_flops = 4 * D * BLOCK * BLOCK * nnz
-    rp2 = layer.lists["cs4a"][0].cpu().numpy()
-    pk, src = peaks()
-    # the attention launch is timed inside a long step (50 x ~1.3 ms of back-to-back kernels):
-    # the sustained (power-capped) cuBLAS figure is the matching denominator; the burst-based
-    # fraction is reported beside it
-    peak_tf = float(pk.get("bf16_tflops_sustained", 1400.0))
-    peak_burst = float(pk.get("bf16_tflops", 1590.0))
-    achieved_tf = alg_flops / (attn_ms * 1e-3) / 1e12
-    exec_tf = exec_flops / (attn_ms * 1e-3) / 1e12
+    cs4a_nnz = int(layer.lists["cs4a"][0][-1].item())
+    alt = sv.SparseLayer(SIDES, K_T, S_D, BLOCK, n_loc, sink_scales=G["sink"],
+                         windows=G["windows"], kinds=("cs4a",), topk=G["topk"], sink_in_source=True)
+    alt.build_patterns(qS, k)
+    cs4a_alt_nnz = int(alt.lists["cs4a"][0][-1].item())
+    del alt
+    # predictor algorithmic bytes per unit: Q_S + K_{<=S} read, the mask and the masses written
+    gS = layer.gs
+    pred_bytes = n_loc * (n_qS * D * 2 + gS["C"] * D * 2 + gS["G_q"] * gS["W"] * 4 +
+                          gS["G_q"] * gS["G_kv"] * 4)
 
-    # --- validation all-gather (untimed): each rank's sampled output rows -> rank 0 (NCCL at
-    # N > 1), where they are compared bit for bit with the same kernel re-run on rank 0 over the
-    # regenerated inputs of that rank's first unit (the kernel is deterministic and launch-
-    # independent: every query tile is computed whole by one CTA in list order)
-    sample_rows = torch.tensor([0, 1, 2047, 4095], device=dev)
-    samp = o_csla[0].index_select(0, sample_rows).float().contiguous()
-    gath = sv_shard.gather_to_root(samp)
+    # --- validation (untimed): all-gather the output shards + patterns, oracle check on rank 0
+    gathered = gather_shards({"o_csla": o_csla, "o_cs4a": o_cs4a, "src": layer.src,
+                              "mapped": layer.mapped, "mass": layer.mass}, n_max)
     validation = None
     if rank == 0:
-        rp1, ci1, st1 = sv.build_block_lists(1, layer.gk["G_q"], layer.gk["G_kv"],
-                                             [(layer.local, True)])
-        mismatch = 0.0
-        for r in range(world):
-            qq = q_iid(0, K_T, r * units, 1, n_q, D, device=dev)
-            kk, vv = kv_cache_iid(0, r * units, 1, n_kv, D, device=dev)
-            oo = sv.block_sparse_attn(SIDES, K_T, BLOCK, qq, kk, vv, rp1, ci1)
-            ref = oo[0].index_select(0, sample_rows).float()
-            mismatch = max(mismatch, float((gath[r].to(dev) - ref).abs().max().item()))
-        validation = {"sampled_rows_max_abs_vs_rank0_rerun": mismatch, "ok": mismatch == 0.0,
-                      "collective": "all_gather_into_tensor" if world > 1 else "none"}
+        gathered = {kk: vv.cpu() for kk, vv in gathered.items()}
+        validation = oracle_check(GEOM, ranges, gathered, units_per_rank=1)
+        validation["collective"] = ("all_gather_into_tensor (NCCL) of every rank's full O shards "
+                                    "and patterns" if world > 1 else "none (1 rank)")
+        validation["gathered_bytes"] = int(sum(t.numel() * t.element_size()
+                                               for t in gathered.values()))
+    del gathered
 
     cpu_baseline = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        t_mask, t_head, n = oracle_sample(0, 0, budget_s=15.0, max_heads=8)
-        cpu_ms = (t_mask + units * t_head) * 1e3 / 2.0
-        # the oracle also checks the sampled output rows of unit 0 (same seeded inputs)
-        from oracle.attention import block_sparse, merge_lists
-        from oracle.csla import local_block_mask
-        from oracle.geometry import Schedule
-        sched = Schedule(SIDES)
-        lists = merge_lists([local_block_mask(sched, K_T, BLOCK, SINK, WINDOWS)])
-        qq = q_iid(0, K_T, 0, 1, n_q, D)[0].double().numpy()
-        kk, vv = kv_cache_iid(0, 0, 1, n_kv, D)
-        rows_u = sorted({int(x) // BLOCK for x in sample_rows.tolist()})
-        want = block_sparse(qq, kk[0].double().numpy(), vv[0].double().numpy(), n_kv, BLOCK, lists,
-                            rows=rows_u)
-        oracle_err = float(np.abs(gath[0].double().cpu().numpy() - want[sample_rows.cpu().numpy()]).max())
-        cpu_baseline = {"value": round(cpu_ms, 2), "unit": "ms/layer", "cores": cpu_cores(),
+        cores = cpu_cores()
+        _limit_blas(cores)
+        r = oracle_units(0, list(range(bh0, bh1)), GEOM, budget_s=20.0, max_units=3)
+        cpu_ms = (r["t_mask"] + units * r["t_sparse_unit"]) * 1e3 / 2.0
+        cpu_dense_ms = units * r["t_dense_unit"] * 1e3
+        cpu_baseline = {"value": round(cpu_ms, 2), "unit": "ms/layer", "cores": cores,
                         "kind": "oracle",
-                        "sample": f"CSLA mask once + predictor/map/merge/2 attentions for {n} of "
-                                  f"{units} (b,h) units, extrapolated to all units",
-                        "oracle_check_sampled_rows_max_abs": oracle_err,
-                        "oracle_check_ok": oracle_err <= 1e-2}
+                        "sample": f"fp64 numpy oracle, BLAS on {cores} threads: CSLA mask once + "
+                                  f"predictor/map/merge/2 block-sparse attentions (O4, O5, O7) "
+                                  f"and the dense attention (O8) for {r['n']} of {units} (b,h) "
+                                  f"units, extrapolated linearly to all units",
+                        "sample_fraction": f"{r['n']}/{units}",
+                        "dense_oracle_ms_per_layer": round(cpu_dense_ms, 2),
+                        "oracle_sparse_vs_dense": round(cpu_dense_ms / cpu_ms, 2)}
 
     if rank == 0:
+        pk, src = peaks()
+        timed_s = ms_step * args.steps / 1e3
+        peak_tf, peak_rule = pick_peak(pk, timed_s, clk)
+        peak_sus = float(pk.get("bf16_tflops_sustained", 1400.0))
+        peak_hbm = float(pk.get("hbm_gbs", 6650.0))
+        achieved_tf = alg_flops / (attn_ms * 1e-3) / 1e12
+        exec_tf = exec_flops / (attn_ms * 1e-3) / 1e12
+        prof = profile_numbers()
+        traffic = prof.get("attn_fwd_kernel")
         value = ms_step / 2.0
+        workload = cfg["name"] + ("" if args.scaling == "strong" else "_weak_per_gpu")
         line = {
             "metric": METRIC, "value": round(value, 4), "unit": "ms/layer", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_step, 4),
-            "higher_is_better": False, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
-            "data": "synthetic (seeded counter-based iid N(0,1), bf16)",
-            "config": {"workload": cfg["name"], "units_bh_per_gpu": units, "batch_per_gpu": cfg["batch"],
+            "higher_is_better": False, "scaling": args.scaling, "vs_baseline": None,
+            "dtype": "bf16", "data": "synthetic (seeded counter-based iid N(0,1), bf16)",
+            "config": {"workload": workload, "units_bh_total": units if args.scaling == "strong"
+                       else units * world, "units_bh_per_gpu": n_loc, "batch": cfg["batch"],
                        "heads": cfg["heads"], "target_scale": K_T, "q_len": n_q, "kv_len": n_kv,
-                       "decision_scale": S_D, "block": BLOCK, "head_dim": D, "sink_scales": SINK,
-                       "windows": list(WINDOWS), "topk": TOPK, "layers_per_step": 2,
-                       "parallelism": f"dp{world} over (batch x head)",
-                       "l2": "inputs > L2 (%.0f MB per GPU)" % ((q.numel() + qS.numel() + 2 * k.numel()) * 2 / 1e6)},
+                       "decision_scale": S_D, "block": BLOCK, "head_dim": D,
+                       "sink_scales": G["sink"], "windows": list(G["windows"]), "topk": G["topk"],
+                       "sink_order": "paper (TopK at S; A_sink U M(TopK) at K)",
+                       "layers_per_step": 2,
+                       "parallelism": f"(batch x head) sharding over {world} GPU(s), "
+                                      f"{args.scaling} scaling, no data-path collective",
+                       "unit_ranges": [list(x) for x in ranges],
+                       "l2": "inputs > L2 (%.0f MB per GPU), no flush" % (
+                           (q.numel() + qS.numel() + 2 * k.numel()) * 2 / 1e6)},
             "roofline": {"bound": "tensor", "kernel": "attn_fwd_kernel<128,128> (CSLA lists)",
                          "achieved": round(achieved_tf, 1), "peak": peak_tf, "unit": "TFLOP/s",
-                         "frac": round(achieved_tf / peak_tf, 4),
-                         "traffic": traffic_from_profile(),
-                         "peak_source": f"{src} bf16_tflops_sustained (kernel timed inside a long step)",
-                         "frac_of_burst_peak": round(achieved_tf / peak_burst, 4),
-                         "flops_per_launch": alg_flops, "launch_ms": round(attn_ms, 4)},
+                         "frac": round(achieved_tf / peak_tf, 4), "traffic": traffic,
+                         "peak_source": f"{src} {peak_rule}",
+                         "frac_of_sustained_peak": round(achieved_tf / peak_sus, 4),
+                         "flops_per_launch": alg_flops, "executed_flops_per_launch": exec_flops,
+                         "launch_ms": round(attn_ms, 4), "launch_ms_max_over_ranks": round(attn_ms_max, 4)},
             "tensor_util_executed": round(exec_tf / peak_tf, 4),
-            "tensor_util_executed_burst": round(exec_tf / peak_burst, 4),
             "csla_attn_ms": round(attn_ms, 4), "dense_attn_ms": round(dense_ms, 4),
             "speedup_vs_dense": round(dense_ms / attn_ms, 3),
-            "csla_active_blocks_per_head": nnz // units,
-            "cs4a_active_blocks_per_head": int(rp2[-1]) // units,
+            "predictor": {"kernel": "predict_kernel<128,128> (S = 11, top-5)",
+                          "ms": round(pred_ms, 4), "algorithmic_bytes": pred_bytes,
+                          "hbm_gbs": round(pred_bytes / (pred_ms * 1e-3) / 1e9, 1),
+                          "frac_of_hbm_peak": round(pred_bytes / (pred_ms * 1e-3) / 1e9 / peak_hbm, 4),
+                          "dram_bytes_ncu": prof.get("predict_kernel"),
+                          "bound": "tensor + MUFU (exp), not HBM: GB/s reported as north_star asks"},
+            "csla_active_blocks_per_head": nnz // n_loc,
+            "cs4a_active_blocks_per_head": cs4a_nnz // n_loc,
+            "cs4a_active_blocks_per_head_sink_in_source": cs4a_alt_nnz // n_loc,
             "e2e": {"value": round(e2e_step / 2.0, 4), "unit": "ms/layer",
                     "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                     "pipelined": "h2d of step i || compute of step i-1 || d2h of step i-2",

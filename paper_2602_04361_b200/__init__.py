@@ -138,6 +138,29 @@ def _bh_view(t: torch.Tensor, name: str):
     return t.stride(0)
 
 
+def _dev_tensor(t, name: str, dtype, min_numel: int = 0, exact_numel: Optional[int] = None):
+    """The C ABI cannot see allocation sizes: check dtype, device, layout and size here."""
+    if not isinstance(t, torch.Tensor) or not t.is_cuda or t.dtype != dtype:
+        raise ValueError(f"{name} must be a CUDA {dtype} tensor")
+    if not t.is_contiguous():
+        raise ValueError(f"{name} must be contiguous")
+    if exact_numel is not None and t.numel() != exact_numel:
+        raise ValueError(f"{name} has {t.numel()} elements, {exact_numel} required")
+    if t.numel() < min_numel:
+        raise ValueError(f"{name} has {t.numel()} elements, at least {min_numel} required")
+    return t
+
+
+def _csr(row_ptr, col_idx, rows: int):
+    """CSR lists of `rows` query blocks: int32 row_ptr[rows + 1] and int32 col_idx."""
+    _dev_tensor(row_ptr, "row_ptr", torch.int32, exact_numel=rows + 1)
+    _dev_tensor(col_idx, "col_idx", torch.int32, min_numel=1)
+
+
+def _kv_rows(sides, scale: int) -> int:
+    return sum(int(s) * int(s) for s in sides[:scale])
+
+
 def geometry(sides: Sequence[int], scale: int, block: int) -> dict:
     """Sizes of scale `scale` (1-based): N, C, G_q, G_kv and the bit-row width W."""
     N = sides[scale - 1] ** 2
@@ -172,10 +195,17 @@ def predict_pattern(sides, decision_scale: int, block: int, sink_scales: int, q_
     g = geometry(sides, decision_scale, block)
     bh, D = q_S.shape[0], q_S.shape[2]
     sh = _Shape(bh, D, _bh_view(q_S, "q_S"), _bh_view(k_cache, "k_cache"), 0)
+    if k_cache.shape[0] < bh or k_cache.shape[1] < g["C"] or k_cache.shape[2] != D:
+        raise ValueError(f"k_cache must be (>= {bh}, >= {g['C']}, {D})")
+    if q_S.shape[1] < g["N"]:
+        raise ValueError(f"q_S needs >= {g['N']} rows")
     if mask_out is None:
         mask_out = torch.empty((bh, g["G_q"], g["W"]), dtype=torch.int32, device="cuda")
     if want_mass and mass_out is None:
         mass_out = torch.empty((bh, g["G_q"], g["G_kv"]), dtype=torch.float32, device="cuda")
+    _dev_tensor(mask_out, "mask_out", torch.int32, min_numel=bh * g["G_q"] * g["W"])
+    if want_mass:
+        _dev_tensor(mass_out, "mass_out", torch.float32, min_numel=bh * g["G_q"] * g["G_kv"])
     _check(lib.sparvar_predict_pattern(ctypes.byref(_sched(sides)), decision_scale, block,
                                        sink_scales, ctypes.byref(sh), _ptr(q_S), _ptr(k_cache),
                                        softmax_scale, mode, topk, threshold,
@@ -188,8 +218,11 @@ def map_indices(sides, src_scale: int, dst_scale: int, block: int, sink_scales: 
                 src_mask: torch.Tensor, mode: int = MAP_FOOTPRINT, out=None, stream=None):
     bh = src_mask.shape[0]
     g = geometry(sides, dst_scale, block)
+    gs = geometry(sides, src_scale, block)
+    _dev_tensor(src_mask, "src_mask", torch.int32, min_numel=bh * gs["G_q"] * gs["W"])
     if out is None:
         out = torch.empty((bh, g["G_q"], g["W"]), dtype=torch.int32, device="cuda")
+    _dev_tensor(out, "out", torch.int32, min_numel=bh * g["G_q"] * g["W"])
     _check(lib.sparvar_map_indices(ctypes.byref(_sched(sides)), src_scale, dst_scale, block,
                                    sink_scales, mode, bh, _ptr(src_mask), _ptr(out),
                                    _stream(stream)))
@@ -209,6 +242,14 @@ def build_block_lists(bh: int, g_q: int, g_kv: int, masks: Sequence[Tuple[torch.
         col_idx = torch.empty(max(1, capacity), dtype=torch.int32, device="cuda")
     if status is None:
         status = torch.zeros(1, dtype=torch.int32, device="cuda")
+    W = -(-g_kv // 32)
+    for i, (m, bc) in enumerate(masks):
+        _dev_tensor(m, f"masks[{i}]", torch.int32, min_numel=(1 if bc else bh) * g_q * W)
+    _dev_tensor(row_ptr, "row_ptr", torch.int32, min_numel=bh * g_q + 1)
+    _dev_tensor(col_idx, "col_idx", torch.int32, min_numel=min(max(1, capacity), 1))
+    if col_idx.numel() < capacity:
+        raise ValueError(f"col_idx has {col_idx.numel()} elements < capacity {capacity}")
+    _dev_tensor(status, "status", torch.int32, min_numel=1)
     ptrs = (ctypes.c_void_p * len(masks))(*[m.data_ptr() for m, _ in masks])
     bc = (ctypes.c_int32 * len(masks))(*[1 if b else 0 for _, b in masks])
     _check(lib.sparvar_build_block_lists(bh, g_q, g_kv, ptrs, bc, len(masks), _ptr(row_ptr),
@@ -216,9 +257,35 @@ def build_block_lists(bh: int, g_q: int, g_kv: int, masks: Sequence[Tuple[torch.
     return row_ptr, col_idx, status
 
 
-def _attn_shape(q, k, o):
-    return _Shape(q.shape[0], q.shape[2], _bh_view(q, "q"), _bh_view(k, "k_cache"),
-                  _bh_view(o, "o"))
+def _attn_shape(q, k, o, v=None, kv_rows: Optional[int] = None, n_q: Optional[int] = None):
+    """Shape struct of an attention call, after checking every tensor against q's (b,h) count:
+    K/V/O with fewer (b,h) slabs (e.g. GQA-shaped K/V) or K/V with fewer than kv_rows rows
+    would make the kernels' TMA / loads read past the allocations."""
+    qs, ks, os_ = _bh_view(q, "q"), _bh_view(k, "k_cache"), _bh_view(o, "o")
+    bh, D = q.shape[0], q.shape[2]
+    for t, name in ((k, "k_cache"), (o, "o")) + (((v, "v_cache"),) if v is not None else ()):
+        if t.shape[0] < bh or t.shape[2] != D:
+            raise ValueError(f"{name} must be (>= {bh}, rows, {D}) like q")
+    if v is not None and _bh_view(v, "v_cache") != ks:
+        raise ValueError("k_cache and v_cache must share a (b,h) stride")
+    if kv_rows is not None:
+        for t, name in ((k, "k_cache"), (v, "v_cache")):
+            if t is not None and t.shape[1] < kv_rows:
+                raise ValueError(f"{name} has {t.shape[1]} rows, the call reads {kv_rows}")
+    if n_q is not None and (q.shape[1] < n_q or o.shape[1] < n_q):
+        raise ValueError(f"q / o need >= {n_q} rows")
+    return _Shape(bh, D, qs, ks, os_)
+
+
+def _cache_in(o_cache, bh: int, n_S: int, D: int):
+    _bh_view(o_cache, "o_cache")
+    if o_cache.shape[0] < bh or o_cache.shape[1] < n_S or o_cache.shape[2] != D:
+        raise ValueError(f"o_cache must be (>= {bh}, >= {n_S}, {D})")
+
+
+def _lse(lse, bh: int, n_q: int):
+    if lse is not None:
+        _dev_tensor(lse, "lse", torch.float32, min_numel=bh * n_q)
 
 
 def block_sparse_attn(sides, target: int, block: int, q: torch.Tensor, k_cache: torch.Tensor,
@@ -226,9 +293,10 @@ def block_sparse_attn(sides, target: int, block: int, q: torch.Tensor, k_cache: 
                       softmax_scale: float = 0.0, o=None, lse=None, stream=None):
     if o is None:
         o = torch.empty_like(q)
-    if _bh_view(v_cache, "v_cache") != k_cache.stride(0):
-        raise ValueError("k_cache and v_cache must share a (b,h) stride")
-    sh = _attn_shape(q, k_cache, o)
+    g = geometry(sides, target, block)
+    sh = _attn_shape(q, k_cache, o, v_cache, g["C"], g["N"])
+    _csr(row_ptr, col_idx, q.shape[0] * g["G_q"])
+    _lse(lse, q.shape[0], g["N"])
     _check(lib.sparvar_block_sparse_attn(ctypes.byref(_sched(sides)), target, block,
                                          ctypes.byref(sh), _ptr(q), _ptr(k_cache), _ptr(v_cache),
                                          _ptr(row_ptr), _ptr(col_idx), softmax_scale, _ptr(o),
@@ -240,9 +308,9 @@ def dense_attn(sides, target: int, q, k_cache, v_cache, softmax_scale: float = 0
                lse=None, stream=None):
     if o is None:
         o = torch.empty_like(q)
-    if _bh_view(v_cache, "v_cache") != k_cache.stride(0):
-        raise ValueError("k_cache and v_cache must share a (b,h) stride")
-    sh = _attn_shape(q, k_cache, o)
+    g = geometry(sides, target, 128)
+    sh = _attn_shape(q, k_cache, o, v_cache, g["C"], g["N"])
+    _lse(lse, q.shape[0], g["N"])
     _check(lib.sparvar_dense_attn(ctypes.byref(_sched(sides)), target, ctypes.byref(sh), _ptr(q),
                                   _ptr(k_cache), _ptr(v_cache), softmax_scale, _ptr(o), _ptr(lse),
                                   _stream(stream)))
@@ -257,11 +325,12 @@ def cache_residual(sides, decision_scale: int, block: int, q_S, k_cache, v_cache
         o_cache = torch.empty_like(q_S)
     if o_scratch is None:
         o_scratch = torch.empty_like(q_S)
-    if _bh_view(v_cache, "v_cache") != k_cache.stride(0):
-        raise ValueError("k_cache and v_cache must share a (b,h) stride")
     if o_scratch.stride(0) != o_cache.stride(0):
         raise ValueError("o_scratch and o_cache must share a (b,h) stride")
-    sh = _attn_shape(q_S, k_cache, o_cache)
+    g = geometry(sides, decision_scale, block)
+    sh = _attn_shape(q_S, k_cache, o_cache, v_cache, g["C"], g["N"])
+    _attn_shape(q_S, k_cache, o_scratch, v_cache, g["C"], g["N"])
+    _csr(row_ptr_S, col_idx_S, q_S.shape[0] * g["G_q"])
     _check(lib.sparvar_cache_residual(ctypes.byref(_sched(sides)), decision_scale, block,
                                       ctypes.byref(sh), _ptr(q_S), _ptr(k_cache), _ptr(v_cache),
                                       _ptr(row_ptr_S), _ptr(col_idx_S), softmax_scale,
@@ -276,11 +345,12 @@ def cache_residual_from_dense(sides, decision_scale: int, block: int, q_S, k_cac
     output instead of recomputing it."""
     if o_cache is None:
         o_cache = torch.empty_like(q_S)
-    if _bh_view(v_cache, "v_cache") != k_cache.stride(0):
-        raise ValueError("k_cache and v_cache must share a (b,h) stride")
     if _bh_view(o_dense, "o_dense") != o_cache.stride(0):
         raise ValueError("o_dense and o_cache must share a (b,h) stride")
-    sh = _attn_shape(q_S, k_cache, o_cache)
+    g = geometry(sides, decision_scale, block)
+    sh = _attn_shape(q_S, k_cache, o_cache, v_cache, g["C"], g["N"])
+    _attn_shape(q_S, k_cache, o_dense, v_cache, g["C"], g["N"])
+    _csr(row_ptr_S, col_idx_S, q_S.shape[0] * g["G_q"])
     _check(lib.sparvar_cache_residual_from_dense(
         ctypes.byref(_sched(sides)), decision_scale, block, ctypes.byref(sh), _ptr(q_S),
         _ptr(k_cache), _ptr(v_cache), _ptr(row_ptr_S), _ptr(col_idx_S), softmax_scale,
@@ -298,8 +368,6 @@ def dense_attn_mass(sides, decision_scale: int, block: int, sink_scales: int, q_
     bh = q_S.shape[0]
     if o is None:
         o = torch.empty_like(q_S)
-    if _bh_view(v_cache, "v_cache") != k_cache.stride(0):
-        raise ValueError("k_cache and v_cache must share a (b,h) stride")
     if mask_out is None:
         mask_out = torch.empty((bh, g["G_q"], g["W"]), dtype=torch.int32, device="cuda")
     if want_mass and mass_out is None:
@@ -307,7 +375,12 @@ def dense_attn_mass(sides, decision_scale: int, block: int, sink_scales: int, q_
     need = dense_attn_mass_workspace(sides, decision_scale, block, bh)
     if workspace is None:
         workspace = torch.empty(max(1, need), dtype=torch.uint8, device="cuda")
-    sh = _attn_shape(q_S, k_cache, o)
+    sh = _attn_shape(q_S, k_cache, o, v_cache, g["C"], g["N"])
+    _lse(lse, bh, g["N"])
+    _dev_tensor(mask_out, "mask_out", torch.int32, min_numel=bh * g["G_q"] * g["W"])
+    if want_mass:
+        _dev_tensor(mass_out, "mass_out", torch.float32, min_numel=bh * g["G_q"] * g["G_kv"])
+    _dev_tensor(workspace, "workspace", torch.uint8)     # size: checked by the ABI (CAPACITY)
     _check(lib.sparvar_dense_attn_mass(
         ctypes.byref(_sched(sides)), decision_scale, block, sink_scales, ctypes.byref(sh),
         _ptr(q_S), _ptr(k_cache), _ptr(v_cache), softmax_scale, mode, topk, threshold, _ptr(o),
@@ -331,6 +404,12 @@ def token_colsum(sides, decision_scale: int, C: int, q_S, k_cache, lse_S, softma
     if out is None:
         out = torch.empty((bh, -(-N // C), Ck), dtype=torch.float32, device="cuda")
     sh = _Shape(bh, D, _bh_view(q_S, "q_S"), _bh_view(k_cache, "k_cache"), 0)
+    if k_cache.shape[0] < bh or k_cache.shape[1] < Ck or q_S.shape[1] < N:
+        raise ValueError("k_cache / q_S too small for the decision scale")
+    _lse(lse_S, bh, N)
+    if lse_S is None:
+        raise ValueError("lse_S is required")
+    _dev_tensor(out, "out", torch.float32, min_numel=bh * -(-N // C) * Ck)
     _check(lib.sparvar_token_colsum(ctypes.byref(_sched(sides)), decision_scale, C,
                                     ctypes.byref(sh), _ptr(q_S), _ptr(k_cache), _ptr(lse_S),
                                     softmax_scale, _ptr(out), _stream(stream)))
@@ -340,8 +419,12 @@ def token_colsum(sides, decision_scale: int, C: int, q_S, k_cache, lse_S, softma
 def token_select(sides, decision_scale: int, C: int, sink_scales: int, colsum, topk_tokens: int,
                  out=None, stream=None):
     bh, G, Ck = colsum.shape
+    if G != -(-(sides[decision_scale - 1] ** 2) // C) or Ck != _kv_rows(sides, decision_scale):
+        raise ValueError("colsum must be (bh, ceil(N_S / C), C_S)")
+    _dev_tensor(colsum, "colsum", torch.float32)
     if out is None:
         out = torch.empty((bh, G, -(-Ck // 32)), dtype=torch.int32, device="cuda")
+    _dev_tensor(out, "out", torch.int32, min_numel=bh * G * -(-Ck // 32))
     _check(lib.sparvar_token_select(ctypes.byref(_sched(sides)), decision_scale, C, sink_scales, bh,
                                     _ptr(colsum), topk_tokens, _ptr(out), _stream(stream)))
     return out
@@ -352,8 +435,12 @@ def token_map(sides, src_scale: int, dst_scale: int, C: int, sink_scales: int, s
     bh = src_mask.shape[0]
     G_K = -(-(sides[dst_scale - 1] ** 2) // C)
     Ck = sum(s * s for s in sides[:dst_scale])
+    G_S = -(-(sides[src_scale - 1] ** 2) // C)
+    _dev_tensor(src_mask, "src_mask", torch.int32,
+                min_numel=bh * G_S * -(-_kv_rows(sides, src_scale) // 32))
     if out is None:
         out = torch.empty((bh, G_K, -(-Ck // 32)), dtype=torch.int32, device="cuda")
+    _dev_tensor(out, "out", torch.int32, min_numel=bh * G_K * -(-Ck // 32))
     _check(lib.sparvar_token_map(ctypes.byref(_sched(sides)), src_scale, dst_scale, C, sink_scales,
                                  mode, bh, _ptr(src_mask), _ptr(out), _stream(stream)))
     return out
@@ -363,9 +450,9 @@ def token_sparse_attn(sides, target: int, C: int, q, k_cache, v_cache, row_ptr, 
                       softmax_scale: float = 0.0, o=None, stream=None):
     if o is None:
         o = torch.empty_like(q)
-    if _bh_view(v_cache, "v_cache") != k_cache.stride(0):
-        raise ValueError("k_cache and v_cache must share a (b,h) stride")
-    sh = _attn_shape(q, k_cache, o)
+    n_q = sides[target - 1] ** 2
+    sh = _attn_shape(q, k_cache, o, v_cache, _kv_rows(sides, target), n_q)
+    _csr(row_ptr, col_idx, q.shape[0] * -(-n_q // C))
     _check(lib.sparvar_token_sparse_attn(ctypes.byref(_sched(sides)), target, C, ctypes.byref(sh),
                                          _ptr(q), _ptr(k_cache), _ptr(v_cache), _ptr(row_ptr),
                                          _ptr(col_idx), softmax_scale, _ptr(o), _stream(stream)))
@@ -380,7 +467,10 @@ def token_cache_residual(sides, decision_scale: int, C: int, q_S, k_cache, v_cac
         o_cache = torch.empty_like(q_S)
     if _bh_view(o_dense, "o_dense") != o_cache.stride(0):
         raise ValueError("o_dense and o_cache must share a (b,h) stride")
-    sh = _attn_shape(q_S, k_cache, o_cache)
+    n_q = sides[decision_scale - 1] ** 2
+    sh = _attn_shape(q_S, k_cache, o_cache, v_cache, _kv_rows(sides, decision_scale), n_q)
+    _attn_shape(q_S, k_cache, o_dense, v_cache, _kv_rows(sides, decision_scale), n_q)
+    _csr(row_ptr_S, col_idx_S, q_S.shape[0] * -(-n_q // C))
     _check(lib.sparvar_token_cache_residual(
         ctypes.byref(_sched(sides)), decision_scale, C, ctypes.byref(sh), _ptr(q_S), _ptr(k_cache),
         _ptr(v_cache), _ptr(row_ptr_S), _ptr(col_idx_S), softmax_scale, _ptr(o_dense),
@@ -395,7 +485,10 @@ def token_sparse_attn_cached(sides, target: int, C: int, q, k_cache, v_cache, ro
     if o is None:
         o = torch.empty_like(q)
     cstride = _bh_view(o_cache, "o_cache")
-    sh = _attn_shape(q, k_cache, o)
+    n_q = sides[target - 1] ** 2
+    sh = _attn_shape(q, k_cache, o, v_cache, _kv_rows(sides, target), n_q)
+    _csr(row_ptr, col_idx, q.shape[0] * -(-n_q // C))
+    _cache_in(o_cache, q.shape[0], sides[cache_scale - 1] ** 2, q.shape[2])
     _check(lib.sparvar_token_sparse_attn_cached(
         ctypes.byref(_sched(sides)), target, C, ctypes.byref(sh), _ptr(q), _ptr(k_cache),
         _ptr(v_cache), _ptr(row_ptr), _ptr(col_idx), softmax_scale, _ptr(o_cache), cache_scale,
@@ -422,8 +515,12 @@ def compress_kv(sides, target: int, cache, sink_scales: int = 5, windows=(7, 5, 
     """(bh, >= C_K, D) bf16 cache -> (bh, kept, D): the CSLA layer's sink + local scales."""
     bh, _, D = cache.shape
     kept = csla_kept_rows(sides, target, sink_scales, windows)
+    if cache.shape[1] < _kv_rows(sides, target):
+        raise ValueError(f"cache needs >= {_kv_rows(sides, target)} rows")
     if out is None:
         out = torch.empty((bh, kept, D), dtype=cache.dtype, device=cache.device)
+    if out.shape[0] < bh or out.shape[1] < kept or out.shape[2] != D:
+        raise ValueError(f"out must be (>= {bh}, >= {kept}, {D})")
     _check(lib.sparvar_compress_kv(ctypes.byref(_sched(sides)), target, sink_scales, _win(windows),
                                    len(windows), bh, D, _ptr(cache), _bh_view(cache, "cache"),
                                    _ptr(out), _bh_view(out, "out"), _stream(stream)))
@@ -449,9 +546,10 @@ def block_sparse_attn_rows(sides, target: int, block: int, q, k_cache, v_cache, 
     """block_sparse_attn over a cache with kv_rows valid rows (e.g. the compressed cache)."""
     if o is None:
         o = torch.empty_like(q)
-    if _bh_view(v_cache, "v_cache") != k_cache.stride(0):
-        raise ValueError("k_cache and v_cache must share a (b,h) stride")
-    sh = _attn_shape(q, k_cache, o)
+    g = geometry(sides, target, block)
+    sh = _attn_shape(q, k_cache, o, v_cache, int(kv_rows), g["N"])
+    _csr(row_ptr, col_idx, q.shape[0] * g["G_q"])
+    _lse(lse, q.shape[0], g["N"])
     _check(lib.sparvar_block_sparse_attn_rows(ctypes.byref(_sched(sides)), target, block,
                                               ctypes.byref(sh), _ptr(q), _ptr(k_cache),
                                               _ptr(v_cache), kv_rows, _ptr(row_ptr), _ptr(col_idx),
@@ -465,10 +563,12 @@ def block_sparse_attn_cached(sides, target: int, block: int, q, k_cache, v_cache
     """NEXT(1): O^(K) = NN-upsample(O_cache) + Delta O^(K), fused epilogue."""
     if o is None:
         o = torch.empty_like(q)
-    if _bh_view(v_cache, "v_cache") != k_cache.stride(0):
-        raise ValueError("k_cache and v_cache must share a (b,h) stride")
     cstride = _bh_view(o_cache, "o_cache")
-    sh = _attn_shape(q, k_cache, o)
+    g = geometry(sides, target, block)
+    sh = _attn_shape(q, k_cache, o, v_cache, g["C"], g["N"])
+    _csr(row_ptr, col_idx, q.shape[0] * g["G_q"])
+    _lse(lse, q.shape[0], g["N"])
+    _cache_in(o_cache, q.shape[0], sides[cache_scale - 1] ** 2, q.shape[2])
     _check(lib.sparvar_block_sparse_attn_cached(
         ctypes.byref(_sched(sides)), target, block, ctypes.byref(sh), _ptr(q), _ptr(k_cache),
         _ptr(v_cache), _ptr(row_ptr), _ptr(col_idx), softmax_scale, _ptr(o_cache), cache_scale,
@@ -518,12 +618,13 @@ class SparseLayer:
         self.status = torch.zeros(1, dtype=torch.int32, device=dev)
         self.cap = cap
 
-    def build_patterns(self, q_S, k_cache, stream=None):
-        """a1-a5: CSLA mask, decision-scale prediction, mapping, and the three CSR list sets."""
+    def build_patterns(self, q_S, k_cache, stream=None, predict: bool = True):
+        """a1-a5: CSLA mask, decision-scale prediction, mapping, and the CSR list sets.
+        predict=False reuses the S-level pattern already in self.src (bench.py times the
+        predictor launch on its own)."""
         local_mask(self.sides, self.K, self.B, self.sink, self.windows, out=self.local, stream=stream)
-        predict_pattern(self.sides, self.S, self.B, self.sink_S, q_S, k_cache, self.select_mode,
-                        self.topk, self.threshold, mask_out=self.src, mass_out=self.mass,
-                        stream=stream)
+        if predict:
+            self.predict(q_S, k_cache, stream)
         map_indices(self.sides, self.S, self.K, self.B, self.sink, self.src, self.map_mode,
                     out=self.mapped, stream=stream)
         g = self.gk
@@ -531,6 +632,12 @@ class SparseLayer:
             rp, ci = self.lists[name]
             build_block_lists(self.bh, g["G_q"], g["G_kv"], self._masks(name), self.cap, rp, ci,
                               self.status, stream=stream)
+
+    def predict(self, q_S, k_cache, stream=None):
+        """a2/a3: the S-level pattern (Top-K alone unless sink_in_source, READING 25)."""
+        predict_pattern(self.sides, self.S, self.B, self.sink_S, q_S, k_cache, self.select_mode,
+                        self.topk, self.threshold, mask_out=self.src, mass_out=self.mass,
+                        stream=stream)
 
     def _masks(self, which):
         return {"csla": [(self.local, True)], "cs4a": [(self.mapped, False)],

@@ -366,6 +366,11 @@ static sparvar_status attn_common(const sparvar_schedule* sched, int32_t target_
   const long long n_kv = n_kv_rows >= 0 ? n_kv_rows : g.cum[target_scale];
   if (n_kv < 1 || n_kv > g.cum[target_scale])
     return fail(SPARVAR_ERR_INVALID_ARG, "kv rows %lld not in [1, C_K]", n_kv);
+  // a tile's KV step count is kept in 16 bits by the kernel (attention.cu, Small::n): with at
+  // most ceil(n_kv / block) steps per tile, bound that here
+  if (ceil_div(n_kv, block) > sv::kMaxKvSteps)
+    return fail(SPARVAR_ERR_UNSUPPORTED, "%d KV blocks of %d rows exceed the kernel's %d steps per "
+                "tile", ceil_div(n_kv, block), block, sv::kMaxKvSteps);
   s = check_shape(shape, n_q, n_kv, true);
   if (s != SPARVAR_OK) return s;
   if (q == nullptr || k == nullptr || v == nullptr || o == nullptr)
@@ -623,11 +628,13 @@ sparvar_status sparvar_token_sparse_attn_cached(
     const uint16_t* o_cache, int32_t cache_scale, int64_t cache_stride_bh, uint16_t* o,
     void* stream) {
   if (o_cache == nullptr) return fail(SPARVAR_ERR_INVALID_ARG, "null o_cache");
-  if (sched == nullptr || cache_scale < 1 || cache_scale > target_scale ||
-      cache_scale > sched->num_scales)
+  sv::Geo g;
+  sparvar_status s = make_geo(sched, &g);          // validates the schedule before any read
+  if (s != SPARVAR_OK) return s;
+  if (cache_scale < 1 || cache_scale > target_scale || cache_scale > g.K)
     return fail(SPARVAR_ERR_INVALID_ARG, "cache_scale %d not in [1, target_scale]", cache_scale);
   if (shape == nullptr) return fail(SPARVAR_ERR_INVALID_ARG, "null shape");
-  const long long n_S = (long long)sched->sides[cache_scale - 1] * sched->sides[cache_scale - 1];
+  const long long n_S = (long long)g.side[cache_scale - 1] * g.side[cache_scale - 1];
   if (cache_stride_bh < n_S * shape->head_dim || cache_stride_bh % 8 != 0 || !aligned16(o_cache))
     return fail(SPARVAR_ERR_INVALID_ARG, "cache_stride_bh must be >= N_S*D, a multiple of 8, "
                 "and o_cache 16-byte aligned");
@@ -704,11 +711,13 @@ sparvar_status sparvar_block_sparse_attn_cached(
     void* stream) {
   if (row_ptr == nullptr || col_idx == nullptr || o_cache == nullptr)
     return fail(SPARVAR_ERR_INVALID_ARG, "null row_ptr / col_idx / o_cache");
-  if (sched == nullptr || cache_scale < 1 || cache_scale > target_scale ||
-      cache_scale > sched->num_scales)
+  sv::Geo g;
+  sparvar_status s = make_geo(sched, &g);          // validates the schedule before any read
+  if (s != SPARVAR_OK) return s;
+  if (cache_scale < 1 || cache_scale > target_scale || cache_scale > g.K)
     return fail(SPARVAR_ERR_INVALID_ARG, "cache_scale %d not in [1, target_scale]", cache_scale);
   if (shape == nullptr) return fail(SPARVAR_ERR_INVALID_ARG, "null shape");
-  const long long n_S = (long long)sched->sides[cache_scale - 1] * sched->sides[cache_scale - 1];
+  const long long n_S = (long long)g.side[cache_scale - 1] * g.side[cache_scale - 1];
   if (cache_stride_bh < n_S * shape->head_dim || cache_stride_bh % 8 != 0 || !aligned16(o_cache))
     return fail(SPARVAR_ERR_INVALID_ARG, "cache_stride_bh must be >= N_S*D, a multiple of 8, "
                 "and o_cache 16-byte aligned");

@@ -157,9 +157,10 @@ __host__ __device__ inline int gcd_int(int a, int b) {
 }
 
 // Small shared state after the Q / KV buffers.
+static_assert(kMaxKvSteps <= 0xFFFF, "Small::n holds a tile's KV step count in 16 bits");
 struct Small {
   float2 stats[2][BM];          // per slot, per row: (1/l or 0, lse) handed softmax -> epilogue
-  uint16_t n[MAX_TILES];        // KV steps of the batch's i-th tile
+  uint16_t n[MAX_TILES];        // KV steps of the batch's i-th tile (<= kMaxKvSteps, api.cu)
   uint8_t meta[MAX_TILES];      // slot | buf << 1 | (use parity of buf) << 3, or EMPTY_TILE
   uint8_t eord[MAX_TILES];      // completion order (for the epilogue)
   int T, Tn, lo, hi, uses;

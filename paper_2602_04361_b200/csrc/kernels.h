@@ -8,6 +8,9 @@
 namespace sv {
 
 constexpr int kMaxScales = 32;
+// attention kernel: a tile's KV step count is stored in 16 bits (attention.cu, Small::n);
+// api.cu rejects ceil(n_kv / block) above this
+constexpr int kMaxKvSteps = 65535;
 
 // Scale geometry copied by value into kernels (a few hundred bytes of kernel parameters).
 struct Geo {

@@ -7,9 +7,12 @@ collective.  Inputs are regenerated per rank from the counter-based generator in
 single-process run bit for bit.  The only collectives are off the timed path:
 
   * `max_over_ranks`: per-rank device times -> the job time (max over ranks);
-  * `gather_to_root`: sampled output rows of every rank -> rank 0, for validation (bench.py
-    compares them with the kernel re-run on rank 0; all_gather_into_tensor over NCCL on the GPU
-    box; gloo in the CPU tests).
+  * `gather_to_root`: a tensor of every rank -> rank 0 (all_gather_into_tensor over NCCL on the
+    GPU box; gloo in the CPU tests).  bench.py gathers every rank's full output shards this way
+    (padded to the largest shard) and checks sampled units of every rank against the oracle.
+
+bench.py's default is strong scaling (`strong_units_ranges`): BASELINE.json configs[3]'s fixed
+96-unit (batch 4 x 24 heads) job split over 1/2/4/8 GPUs.
 """
 from __future__ import annotations
 
@@ -18,7 +21,7 @@ from typing import List, Optional, Tuple
 import torch
 import torch.distributed as dist
 
-__all__ = ["weak_units", "strong_units", "max_over_ranks", "gather_to_root"]
+__all__ = ["weak_units", "strong_units", "strong_units_ranges", "max_over_ranks", "gather_to_root"]
 
 
 def weak_units(rank: int, units_per_rank: int) -> Tuple[int, int]:
@@ -33,6 +36,13 @@ def strong_units(rank: int, world: int, total_units: int) -> Tuple[int, int]:
     if not 0 <= rank < world:
         raise ValueError("0 <= rank < world required")
     return rank * total_units // world, (rank + 1) * total_units // world
+
+
+def strong_units_ranges(world: int, total_units: int) -> List[Tuple[int, int]]:
+    """Every rank's strong-scaling range (rank r takes [r*U/g, (r+1)*U/g))."""
+    if world < 1 or total_units < world:
+        raise ValueError("need 1 <= world <= total_units")
+    return [strong_units(r, world, total_units) for r in range(world)]
 
 
 def max_over_ranks(values: List[float], device=None) -> List[float]:

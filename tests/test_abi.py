@@ -144,3 +144,35 @@ def test_next_rows_validation(sv):
     st = sv.lib.sparvar_block_sparse_attn_rows(S4, 4, 16, ctypes.byref(sh), p, p, p, 86, p, p, 0.0,
                                                p, None, None)   # more rows than C_K = 85
     assert st == 1
+
+
+def test_kv_step_bound_and_cached_schedule_checks(sv):
+    """the attention kernel holds a tile's KV step count in 16 bits, so a cache of more
+    than 65535 blocks is rejected up front (UNSUPPORTED); the cached entry points validate the
+    schedule before reading it (a NULL `sides` is INVALID_ARG, not a crash)."""
+    p = ctypes.c_void_p(256)
+    big = _sched(sv, [1024, 1025])                      # C_2 = 2,099,201 rows -> 131,201 blocks
+    sh = sv._Shape(1, 64, 1025 * 1025 * 64, 2099201 * 64, 1025 * 1025 * 64)
+    st = sv.lib.sparvar_block_sparse_attn(big, 2, 16, ctypes.byref(sh), p, p, p, p, p, 0.0, p,
+                                          None, None)
+    assert st == 3 and b"steps per tile" in sv.lib.sparvar_last_error()
+    null = sv._Schedule(2, ctypes.POINTER(ctypes.c_int32)())
+    st = sv.lib.sparvar_block_sparse_attn_cached(ctypes.byref(null), 2, 16, ctypes.byref(sh), p, p,
+                                                 p, p, p, 0.0, p, 1, 64, p, None, None)
+    assert st == 1 and b"null schedule" in sv.lib.sparvar_last_error()
+    st = sv.lib.sparvar_token_sparse_attn_cached(ctypes.byref(null), 2, 64, ctypes.byref(sh), p, p,
+                                                 p, p, p, 0.0, p, 1, 64, p, None)
+    assert st == 1 and b"null schedule" in sv.lib.sparvar_last_error()
+
+
+def test_binding_rejects_bad_tensors(sv):
+    """the Python wrappers check what the C ABI cannot see (allocation sizes, dtypes,
+    devices) before passing raw pointers; CPU tensors and wrong dtypes are refused."""
+    import torch
+    q = torch.zeros((2, 64, 64), dtype=torch.bfloat16)
+    with pytest.raises(ValueError):
+        sv.dense_attn([1, 2, 4, 8], 4, q, q, q)                  # not CUDA
+    with pytest.raises(ValueError):
+        sv._dev_tensor(torch.zeros(4, dtype=torch.int64), "row_ptr", torch.int32)
+    with pytest.raises(ValueError):
+        sv._dev_tensor(torch.zeros(4, dtype=torch.int32), "row_ptr", torch.int32)   # CPU
