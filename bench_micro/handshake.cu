@@ -108,7 +108,7 @@ __global__ void __launch_bounds__(352, 1) k_two(long long* out, int steps) {
       const int s = ring % NST;
       const long long w0 = clock64();
       if (ISSUERS == 3) mbar_wait_spin(kv_full + s, (ring / NST) & 1);
-      else if (ISSUERS == 4 || ISSUERS == 7) { /* no wait: isolates the cost of the loader / commits */ }
+      else if (ISSUERS == 4 || ISSUERS == 7 || ISSUERS == 8 || ISSUERS == 10) { /* no wait: isolates the cost of the loader / commits */ }
       else if (ISSUERS == 5) { if (s == 0) mbar_wait(kv_full + s, (ring / NST) & 1); }
       else mbar_wait(kv_full + s, (ring / NST) & 1);
       wt += clock64() - w0;
@@ -118,13 +118,15 @@ __global__ void __launch_bounds__(352, 1) k_two(long long* out, int steps) {
     return 0;
   };
   auto release = [&](int s) { if (NST > 0) mma_commit(kv_empty + s); };
+  int deferred = -1;   // ISSUERS >= 8: the V stage's release commit moved after the QK group
   auto step_ops = [&](int t, int g, bool pv) {
     if (pv) {
       const int sv = stage();
       const uint32_t vb = kv + ((2 * g + t) % 4) * 32768u;
       for (int kk = 0; kk < 8; ++kk)
         mma_ts(tmem + 256 + t * 128, tmem + t * 128 + kk * 8, sdesc_sw128(vb + kk * 2048, 16384, 1024), idp, 1);
-      release(sv);
+      if (ISSUERS < 8) release(sv);
+      else deferred = sv;
     }
     const int sk = stage();
     const uint32_t kb = kv + ((2 * g + t + 1) % 4) * 32768u;
@@ -132,6 +134,15 @@ __global__ void __launch_bounds__(352, 1) k_two(long long* out, int steps) {
     for (int kk = 0; kk < 8; ++kk)
       mma_ss(tmem + t * 128, sdesc_sw128(qb + (kk >> 2) * 16384 + (kk & 3) * 32, 16, 1024),
              sdesc_sw128(kb + (kk >> 2) * 16384 + (kk & 3) * 32, 16, 1024), idq, kk > 0);
+    if (ISSUERS == 10) {                      // s_full first, then the ring releases
+      mma_commit(s_full + t);
+      if (deferred >= 0) release(deferred);
+      release(sk);
+      deferred = -1;
+      return;
+    }
+    if (deferred >= 0) release(deferred);
+    deferred = -1;
     release(sk);
     mma_commit(s_full + t);
   };
@@ -231,5 +242,9 @@ int main() {
   run_two<5, 8>("two slots, ring, waits on 1 of 8 stages");
   run_two<6, 8>("two slots, ring 8, loader polls");
   run_two<7, 8>("two slots, ring 8, loader active, issuer never waits");
+  run_two<2, 0>("two slots, two issuer warps, no KV ring");
+  run_two<8, 8>("two slots, ring commits deferred, no waits");
+  run_two<9, 8>("two slots, ring 8 + loader, commits deferred");
+  run_two<10, 8>("two slots, ring commits after s_full, no waits");
   return 0;
 }

@@ -37,7 +37,8 @@ for t in "$@"; do
     ncu:*)
       IFS=: read -r _ rx bargs <<< "$t"
       tag=$(echo "$rx" | tr -c 'a-zA-Z0-9_' '_')
-      timeout 1200 ncu --set full --clock-control none --import-source on -k "regex:$rx" -c 1 \
+      timeout 1200 ncu --set full --clock-control none --import-source on -k "regex:$rx" -s 2 -c 1 \
+        --metrics sm__pipe_tensor_subpipe_hmma_cycles_active.avg.pct_of_peak_sustained_elapsed,sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed,sm__inst_executed_pipe_xu.avg.pct_of_peak_sustained_active \
         -f -o gpurun_out/ncu_$tag python bench.py --steps 1 --warmup 3 --no-cpu-baseline \
         $bargs > gpurun_out/ncu_$tag.log 2>&1
       tail -3 gpurun_out/ncu_$tag.log ;;

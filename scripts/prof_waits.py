@@ -33,12 +33,21 @@ a = np.array(buf[:], dtype=np.int64)
 g = lambda base: a[base:base + 148].astype(np.float64)
 ops = g(7000)
 tot = g(6800)
-print(f"{which}: slot-ops per CTA median {np.median(ops):.0f} (min {ops.min():.0f} max {ops.max():.0f})")
+print(f"{os.path.basename(sv.LIB_PATH)} {which}: slot-ops per CTA median {np.median(ops):.0f} (min {ops.min():.0f} max {ops.max():.0f})")
 print(f"  MMA loop clk per op (median CTA): {np.median(tot / np.maximum(ops, 1)):.0f}  "
-      f"(tensor work per op at 100%: {2 * 8 * 64} clk)")
-for name, base in [("MMA wait kv_full", 6000), ("MMA wait P", 6200), ("MMA wait o_free", 6400),
-                   ("MMA wait q_full", 6600), ("loader wait kv_empty", 5000),
-                   ("softmax wait S (2 thr)", 5200), ("epilogue wait O (2 thr)", 5400)]:
+      f"(tensor work per op at 100%: {int(os.environ.get("SV_OP_CLK", "1024"))} clk)")
+LABELS = {
+    "v6": [("MMA wait kv_full", 6000), ("MMA wait P", 6200), ("MMA wait o_free", 6400),
+           ("MMA wait q_full", 6600), ("loader wait kv_empty", 5000),
+           ("softmax wait S (2 thr)", 5200), ("epilogue wait O (2 thr)", 5400),
+           ("MMA issue block P.V", 7200), ("MMA issue block QK", 7400),
+           ("softmax compute (2 thr)", 7600), ("softmax wait prev P.V (8 w)", 7800)],
+    "pairs": [("MMA wait K stage", 6000), ("MMA wait V stage", 5400), ("MMA wait S free", 6200),
+              ("MMA wait P written", 5600), ("MMA wait o_free", 6400), ("MMA wait q_full", 6600),
+              ("loader wait stage empty", 5000), ("softmax wait S (2 thr)", 5200),
+              ("softmax compute (2 thr)", 7600), ("softmax wait P buffer (8 w)", 7800)],
+}[os.environ.get("SV_PROF_LABELS", "v6")]
+for name, base in LABELS:
     v = g(base)
     print(f"  {name:26s} per op {np.median(v / np.maximum(ops, 1)):7.0f} clk   share of MMA loop "
           f"{np.median(v / np.maximum(tot, 1)):.3f}")

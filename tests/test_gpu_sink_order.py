@@ -124,7 +124,10 @@ def test_step_cache_both_orders(sink_in_source):
             assert (src[b].sum(1) == 2).all()
         qb = {k: to_np(qs[k][b]) for k in range(S, K + 1)}
         kb, vb = to_np(kc[b]), to_np(vc[b])
-        oc = cache_residual(qb[S], kb, vb, sched.C(S), B, merge_lists([src[b]]))
+        want_oc = cache_residual(qb[S], kb, vb, sched.C(S), B, merge_lists([src[b]]))
+        oc = to_np(st.o_cache[b])          # the cached kernel's own (bf16) input, checked here
+        mx, mean = attn_errors(oc, want_oc)
+        assert mx <= MAX_ABS and mean <= MEAN_ABS, ("o_cache", mx, mean)
         for k in st.targets:
             want_map = map_pattern(src[b], sched, S, k, B, sink, "footprint")
             got_map = bits_to_bool(st.mapped[k].cpu().numpy(), st.g[k]["G_kv"])[b]

@@ -61,11 +61,16 @@ def test_sparsified_step_parity(step_mod, fused):
             if st.kind(l) == "cs4a":
                 lists_S = merge_lists([src[b]])
                 want_oc = cache_residual(qb[S], kb, vb, sched.C(S), B, lists_S)
+                got_oc = to_np(st.o_cache[b])
+                mx, mean = attn_errors(got_oc, want_oc)
+                assert mx <= MAX_ABS and mean <= MEAN_ABS, ("o_cache", l, mx, mean)
                 for k in st.targets:
                     want_map = map_pattern(src[b], sched, S, k, B, sink, "footprint")
                     assert np.array_equal(mapped[k][b], want_map), ("mapped", l, k)
+                    # the cached kernel's inputs include the bf16 O_cache: compared on the GPU's
+                    # own O_cache, itself checked against the oracle above
                     want = cached_sparse(qb[k], kb, vb, sched.C(k), B, merge_lists([want_map]),
-                                         want_oc, sides[S - 1], sides[k - 1])
+                                         got_oc, sides[S - 1], sides[k - 1])
                     mx, mean = attn_errors(to_np(outs[l][k][b]), want)
                     assert mx <= MAX_ABS and mean <= MEAN_ABS, ("cs4a", l, k, mx, mean)
             else:
@@ -127,7 +132,10 @@ def test_token_granularity_step(step_mod):
         kb, vb = to_np(ks[0][b]), to_np(vs[0][b])
         mx, mean = attn_errors(to_np(outs[0][S][b]), dense(qb[S], kb, vb, sched.C(S)))
         assert mx <= MAX_ABS and mean <= MEAN_ABS
-        oc = token_cache_residual(qb[S], kb, vb, sched.C(S), C, sel[b])
+        want_oc = token_cache_residual(qb[S], kb, vb, sched.C(S), C, sel[b])
+        oc = to_np(st.o_cache[b])
+        mx, mean = attn_errors(oc, want_oc)
+        assert mx <= MAX_ABS and mean <= MEAN_ABS, ("o_cache", mx, mean)
         for k in st.targets:
             got_map = bits_to_bool(st.tmap[k].cpu().numpy(), sched.C(k))[b]
             want_map = map_tokens(sel[b], sched, S, k, C, sink)

@@ -123,7 +123,8 @@ def test_token_cache_path(sv, sides, S, K, C, D, bh, sink, alpha):
         want_oc = token_cache_residual(qb, kb, vb, sched.C(S), C, got_sel[b])
         mx, mean = attn_errors(to_np(oc[b]), want_oc)
         assert mx <= MAX_ABS and mean <= MEAN_ABS, ("o_cache", b, mx, mean)
-        want = token_cached_sparse(to_np(qK[b]), kb, vb, C, got_dst[b], want_oc, sides[S - 1],
+        # the cached kernel's inputs include the bf16 O_cache: compared on the GPU's own
+        want = token_cached_sparse(to_np(qK[b]), kb, vb, C, got_dst[b], to_np(oc[b]), sides[S - 1],
                                    sides[K - 1])
         mx, mean = attn_errors(to_np(o2[b]), want)
         assert mx <= MAX_ABS and mean <= MEAN_ABS, ("O^(K)", b, mx, mean)
