@@ -198,6 +198,9 @@ struct TokCache {
   int s_src, s_dst;
 };
 
+#ifndef SV_TOK_ROW_GATHER
+#define SV_TOK_ROW_GATHER 0   // 1: one list row per lane (round-1 gather), 0: coalesced rows
+#endif
 constexpr int TOK_WARPS = 16;
 constexpr int TOK_THREADS = TOK_WARPS * 32;
 constexpr int TOK_WARP_MMA = 8, TOK_WARP_GATHER0 = 9;
@@ -258,6 +261,7 @@ __global__ void __launch_bounds__(TOK_THREADS, 1) token_attn_kernel(
         const int b = c & 1;
         if (c >= 2) mbar_wait(&kv_empty[b], ((c >> 1) - 1) & 1);
         const uint32_t dK = smem_u32(sK + b * TC::TILE_BYTES), dV = smem_u32(sV + b * TC::TILE_BYTES);
+#if SV_TOK_ROW_GATHER
         for (int i = gw * 32 + lane; i < TBM; i += TOK_GATHER_WARPS * 32) {
           const int e = c * TBM + i;
           const bool ok = e < n;
@@ -271,6 +275,22 @@ __global__ void __launch_bounds__(TOK_THREADS, 1) token_attn_kernel(
             cp_async16(dV + off, vs + p * 8, ok);
           }
         }
+#else
+        // coalesced: the D/8 16-byte pieces of a row go to consecutive lanes, so a warp
+        // instruction reads 32 * 16 B from 32 / (D/8) whole rows (2 at D = 128) instead of one
+        // piece of 32 different rows (32 L1 wavefronts)
+        constexpr int PIECES = D / 8, RPI = 32 / PIECES;         // rows per warp instruction
+        const int p = lane % PIECES, ri = lane / PIECES;
+        for (int i0 = gw * RPI; i0 < TBM; i0 += TOK_GATHER_WARPS * RPI) {
+          const int i = i0 + ri;
+          const int e = c * TBM + i;
+          const bool ok = e < n;
+          const int tok = ok ? __ldg(col_idx + beg + e) : 0;
+          const uint32_t off = (p >> 3) * (TBM * 128) + i * 128 + (((p & 7) ^ (i & 7)) << 4);
+          cp_async16(dK + off, kb + (long long)tok * D + p * 8, ok);
+          cp_async16(dV + off, vb + (long long)tok * D + p * 8, ok);
+        }
+#endif
         cp_async_wait_all();
         fence_proxy_async();
         __syncwarp();
@@ -319,11 +339,14 @@ __global__ void __launch_bounds__(TOK_THREADS, 1) token_attn_kernel(
         __syncwarp();
       };
       for (int c = 0; c < chunks; ++c) {
-        mbar_wait(&kv_full[c & 1], (c >> 1) & 1);
-        tc_fence_after();
 #pragma unroll
         for (int t = 0; t < NS; ++t) {
           if (c > 0) pv(t, c - 1);
+          // P_0,c-1 V_c-1 only needs chunk c-1: issue it before waiting for chunk c's gather
+          if (t == 0) {
+            mbar_wait(&kv_full[c & 1], (c >> 1) & 1);
+            tc_fence_after();
+          }
           qk(t, c);
         }
       }

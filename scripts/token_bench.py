@@ -29,6 +29,8 @@ def main():
     ap.add_argument("--C", type=int, default=192)
     ap.add_argument("--alpha", type=float, default=0.2)
     ap.add_argument("--out", default=None)
+    ap.add_argument("--sink-in-source", action="store_true",
+                    help="OR the sink tokens into the S-level selection (READING 25's alternative)")
     args = ap.parse_args()
     import paper_2602_04361_b200 as sv
     from synth import kv_cache_iid, q_iid
@@ -66,7 +68,8 @@ def main():
     import math
     k_tok = max(1, math.ceil(args.alpha * CS))
     sel = torch.empty((bh, G_S, -(-CS // 32)), dtype=torch.int32, device=dev)
-    t_sel = timed(lambda: sv.token_select(SIDES, S, C, sink, cs, k_tok, out=sel))
+    sink_S = sink if args.sink_in_source else 0          # READING 25: paper order by default
+    t_sel = timed(lambda: sv.token_select(SIDES, S, C, sink_S, cs, k_tok, out=sel))
     dst = torch.empty((bh, G_K, -(-CK // 32)), dtype=torch.int32, device=dev)
     t_map = timed(lambda: sv.token_map(SIDES, S, K, C, sink, sel, out=dst))
     cap = bh * G_K * CK
@@ -89,7 +92,8 @@ def main():
         "metric": "token-granular CS4A (NEXT 2) per-kernel ms", "unit": "ms",
         "config": {"workload": "infinity8b_shape_token_cs4a", "units_bh": bh, "decision_scale": S,
                    "target_scale": K, "query_block_C": C, "alpha": args.alpha, "topk_tokens": k_tok,
-                   "sink_scales": sink, "head_dim": D, "data": "synthetic seeded iid bf16"},
+                   "sink_scales": sink, "head_dim": D, "data": "synthetic seeded iid bf16",
+                   "sink_order": "sink_in_source" if args.sink_in_source else "paper"},
         "dense_attn_S_with_lse_ms": round(t_dense_S, 4),
         "colsum_ms": round(t_col, 4), "colsum_tflops": round(col_flops / t_col / 1e9, 1),
         "colsum_gexp_per_s": round(bh * NS * CS / t_col / 1e6, 1),
