@@ -5,7 +5,7 @@ K=11 with decision scale S=10) and the K=13 last scale, on `structured` syntheti
 Points:
   * CSLA window rows of Table csla_ablation: (a,b,c) on scales 11,12,13,
     scales 9,10 window 1, 6-8 masked; sink <= 5, 6, 7, 8 and none.
-  * Predictor (CS4A lists: sink + mapped) top-k in {2,3,5,7,10} and threshold tau in
+  * Predictor (CS4A lists: sink + mapped, the paper's sink order) top-k in {2,3,5,7,10} and tau in
     {0.005,0.01,0.02,0.05} at S=11 -> K=13 and S=10 -> K=11.
   * Block size B in {64, 128}.
 Each point reports the attention ms (CUDA events, median), listed and executed FLOPs, tensor
@@ -80,7 +80,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--reps", type=int, default=20)
     ap.add_argument("--seed", type=int, default=0)
-    ap.add_argument("--out", default=os.path.join(ROOT, "profiles", "r01_sweep.jsonl"))
+    ap.add_argument("--out", default=os.path.join(ROOT, "gpurun_out", "sweep.jsonl"))
     ap.add_argument("--quick", action="store_true", help="a few points only (smoke)")
     args = ap.parse_args()
 
@@ -160,7 +160,8 @@ def main():
             if args.quick:
                 sels = [("topk", 5)]
             for mode, val in sels:
-                src, _ = sv.predict_pattern(SIDES, S, B, 5, qS, k,
+                # READING 25: Top-K alone at S, the sink added by the map at K
+                src, _ = sv.predict_pattern(SIDES, S, B, 0, qS, k,
                                             sv.SELECT_TOPK if mode == "topk" else sv.SELECT_THRESHOLD,
                                             topk=int(val) if mode == "topk" else 1,
                                             threshold=float(val) if mode == "threshold" else 0.0)
