@@ -34,13 +34,48 @@
 #define SV_PRED_EMU_EVERY 8   // 1 in 8 exp2 pairs as a degree-4 polynomial on the FMA pipe
 #endif
 
+#ifdef SV_PRED_PROF
+// Development instrumentation (variant libraries only, -DSV_PRED_PROF): clocks summed over CTAs.
+__device__ unsigned long long sv_pred_prof[16];
+extern "C" int sparvar_pred_prof_read(unsigned long long* host) {
+  return cudaMemcpyFromSymbol(host, sv_pred_prof, sizeof(sv_pred_prof)) == cudaSuccess ? 0 : 1;
+}
+extern "C" int sparvar_pred_prof_reset() {
+  static unsigned long long z[16];
+  return cudaMemcpyToSymbol(sv_pred_prof, z, sizeof(z)) == cudaSuccess ? 0 : 1;
+}
+#ifdef SV_PRED_TRACE
+// one CTA's timeline: softmax (quarter-0 warp of each slot) wait/body/end per step, the issuer's
+// MMA block per slot-step, tile ends
+__device__ long long sv_pred_tr_sm[2][400][3];
+__device__ long long sv_pred_tr_mma[2][400][2];
+__device__ long long sv_pred_tr_te[2][16][2];
+extern "C" int sparvar_pred_trace_read(long long* sm, long long* mma, long long* te) {
+  return (cudaMemcpyFromSymbol(sm, sv_pred_tr_sm, sizeof(sv_pred_tr_sm)) == cudaSuccess &&
+          cudaMemcpyFromSymbol(mma, sv_pred_tr_mma, sizeof(sv_pred_tr_mma)) == cudaSuccess &&
+          cudaMemcpyFromSymbol(te, sv_pred_tr_te, sizeof(sv_pred_tr_te)) == cudaSuccess) ? 0 : 1;
+}
+#define TR_ON (blockIdx.x == SV_PRED_TRACE)
+#endif
+#define PP_T0() const long long pp0_ = clock64();
+#ifdef SV_PRED_TRACE_ONLY
+#define PP_ATOMIC(i_, v_)
+#else
+#define PP_ATOMIC(i_, v_) atomicAdd(&sv_pred_prof[i_], (unsigned long long)(v_));
+#endif
+#define PP_ADD(i_) if ((threadIdx.x & 31) == 0) { PP_ATOMIC(i_, clock64() - pp0_) }
+#else
+#define PP_T0()
+#define PP_ADD(i_)
+#endif
+
 namespace sv {
 namespace {
 
 constexpr int BM = 128;
-constexpr int NUM_WARPS = 12;            // WG0/WG1 softmax slot 0/1, warp 8 MMA, 9 K, 10 Q
+constexpr int NUM_WARPS = 12;   // WG0/WG1 softmax slot 0/1, warp 8 MMA, 9 K, 10 Q, 11 selection
 constexpr int NUM_THREADS = NUM_WARPS * 32;
-constexpr int WARP_MMA = 8, WARP_K = 9, WARP_Q = 10;
+constexpr int WARP_MMA = 8, WARP_K = 9, WARP_Q = 10, WARP_SEL = 11;
 constexpr int REG_LAUNCH = 168;
 constexpr int REG_SOFTMAX = 208;
 constexpr int REG_OTHER = 88;
@@ -49,7 +84,8 @@ constexpr uint32_t TMEM_COLS = 512;
 constexpr int EMU_EVERY = SV_PRED_EMU_EVERY;
 constexpr int SMEM_LIMIT = 232448;
 constexpr int MAXQ = 4;
-constexpr int NBARS = 2 * MAXQ + 2 * 8 + 8;   // q full/empty, kv full/empty, s full/free [2][2]
+// q full/empty, kv full/empty, s full/free [2][2], part full/free [2][2]
+constexpr int NBARS = 2 * MAXQ + 2 * 8 + 8 + 8;
 
 template <int D, int BLK>
 struct PCfg {
@@ -61,8 +97,8 @@ struct PCfg {
   static constexpr int NSEG = BM / SEG;
   // bytes of everything but the Q buffers and the K ring
   static size_t fixed(int g_kv) {
-    return size_t(2) * g_kv * BM * 4 /* block sums */ + size_t(2) * NSEG * g_kv * 4 /* parts */ +
-           NBARS * 8 + 16;
+    return size_t(2) * g_kv * BM * 4 /* block sums */ + size_t(4) * NSEG * g_kv * 4 /* parts */ +
+           size_t((g_kv + 1) & ~1) * 4 /* selection row */ + NBARS * 8 + 16;
   }
   // (Q buffers, K stages) that fit, preferring 4 Q buffers (both tiles of the next round
   // prefetched); nst = 0 if nothing fits
@@ -90,14 +126,17 @@ predict_kernel(const __grid_constant__ CUtensorMap tmap_q,
   uint8_t* sQ = smem;
   uint8_t* sK = smem + nqb * C::Q_BYTES;
   float* sums = reinterpret_cast<float*>(sK + nst * C::STAGE_BYTES);   // [2][n][BM]
-  float* part = sums + 2 * n * BM;                                      // [2][NSEG][n]
-  uint64_t* bars = reinterpret_cast<uint64_t*>(part + 2 * C::NSEG * n);
+  float* part = sums + 2 * n * BM;                              // [2 slots][2 bufs][NSEG][n]
+  float* sel_row = part + 4 * C::NSEG * n;                      // [n] selection warp's mass row
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sel_row + ((n + 1) & ~1));   // 8-byte aligned
   uint64_t* q_full = bars;           // [MAXQ]
   uint64_t* q_empty = q_full + MAXQ; // [MAXQ]
   uint64_t* kv_full = q_empty + MAXQ;// [8]
   uint64_t* kv_empty = kv_full + 8;  // [8]
   uint64_t* s_full = kv_empty + 8;   // [2 slots][2 bufs]
   uint64_t* s_free = s_full + 4;     // [2 slots][2 bufs] (128 arrivals)
+  uint64_t* part_full = s_free + 4;  // [2 slots][2 bufs] (128 arrivals)
+  uint64_t* part_free = part_full + 4;   // [2 slots][2 bufs]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + NBARS);
 
   const int warp = threadIdx.x >> 5;
@@ -125,6 +164,8 @@ predict_kernel(const __grid_constant__ CUtensorMap tmap_q,
     for (int i = 0; i < 4; ++i) {
       mbar_init(s_full + i, 1);
       mbar_init(s_free + i, BM);
+      mbar_init(part_full + i, BM);
+      mbar_init(part_free + i, 1);
     }
     fence_barrier_init();
   }
@@ -172,7 +213,7 @@ predict_kernel(const __grid_constant__ CUtensorMap tmap_q,
               const int s = idx % nst;
               const uint32_t ph = (idx / nst) & 1;
               ++idx;
-              mbar_wait(kv_empty + s, ph ^ 1);
+              { PP_T0() mbar_wait(kv_empty + s, ph ^ 1); PP_ADD(3) }
               mbar_arrive_expect_tx(kv_full + s, C::STAGE_BYTES);
 #pragma unroll
               for (int x = 0; x < C::NBOX; ++x)
@@ -182,38 +223,104 @@ predict_kernel(const __grid_constant__ CUtensorMap tmap_q,
           }
         }
       }
+    } else if (warp == WARP_SEL) {
+      // ---------------------------------------------------------------- selection
+      // Tile k's per-warp partial masses arrive in part[k & 1][(k >> 1) & 1]; this warp sums the
+      // segments of each query block into its mass row and selects with ballots into bit rows,
+      // off the softmax warps' critical path.
+      const int W = (n + 31) / 32;
+      constexpr int SEG_PER_G = BLK / C::SEG;
+      for (int k = 0; k < T; ++k) {
+        const int t = k & 1, kk = k >> 1, pb = kk & 1;
+        const float* pt = part + (t * 2 + pb) * C::NSEG * n;
+        mbar_wait(part_full + 2 * t + pb, (kk >> 1) & 1);
+        const int it = lo + k;
+        const int bh = it / n_tiles, tile = it % n_tiles;
+        for (int gq = 0; gq < C::G; ++gq) {
+          const int u = tile * C::G + gq;
+          if (u >= a.g_q) break;
+          for (int v = lane; v < n; v += 32) {
+            float acc = 0.f;
+            for (int sgi = 0; sgi < SEG_PER_G; ++sgi) acc += pt[(gq * SEG_PER_G + sgi) * n + v];
+            sel_row[v] = acc;
+          }
+          __syncwarp();
+          const long long r = (long long)bh * a.g_q + u;
+          const int rows_u = min(BLK, a.n_q - u * BLK);
+          const float thr = a.tau * float(rows_u);
+          for (int w0 = 0; w0 < W; ++w0) {
+            const int v = w0 * 32 + lane;
+            bool sel = false;
+            if (v < n) {
+              const float mv = sel_row[v];
+              if (a.mode == 0) {
+                int rank = 0;
+#pragma unroll 8
+                for (int tt = 0; tt < n; ++tt) {
+                  const float mt = sel_row[tt];
+                  rank += (mt > mv) || (mt == mv && tt < v);
+                }
+                sel = rank < a.topk;
+              } else {
+                sel = mv >= thr;
+              }
+              sel = sel || (v < a.n_sink_blocks);
+              if (a.mass) a.mass[r * n + v] = mv;
+            }
+            const uint32_t word = __ballot_sync(0xffffffffu, sel);
+            if (lane == 0) a.mask[r * W + w0] = word;
+          }
+          __syncwarp();   // sel_row is rewritten by the next query block
+        }
+        if (lane == 0) mbar_arrive(part_free + 2 * t + pb);
+      }
     } else if (warp == WARP_MMA) {
       // ---------------------------------------------------------------- tcgen05 issuer
       constexpr uint32_t IDESC = idesc_bf16_f32(BM, BLK, 0, 0);
       const bool leader = elect_one();
       const uint64_t dq0 = sdesc_sw128(smem_u32(sQ), 16, 1024);
       const uint64_t dk0 = sdesc_sw128(smem_u32(sK), 16, 1024);
-      int idx = 0;
+      // ring positions and Q buffer indices as incremental counters: no integer division on the
+      // issue path (the issuer shares its SM sub-partition with two softmax warps)
+      int ring_s = 0;
+      uint32_t ring_ph = 0;
+      int qbuf = 0;                        // Q buffer of slot use k = 2r (round r's first tile)
+      uint32_t qph = 0;                    // its use parity
       uint32_t step0 = 0, step1 = 0;   // S buffer uses per slot
+      PP_T0()
       for (int r = 0; 2 * r < T; ++r) {
         const bool two = 2 * r + 1 < T;
         const bool shared = two && (lo + 2 * r + 1) / n_tiles == (lo + 2 * r) / n_tiles;
+        // Q buffers of the round's tiles (use k = 2r + t: buffer k % nqb, parity (k / nqb) & 1)
+        int qb[2];
+        uint32_t qp[2];
+        qb[0] = qbuf;
+        qp[0] = qph;
+        qb[1] = qbuf + 1 == nqb ? 0 : qbuf + 1;
+        qp[1] = qbuf + 1 == nqb ? qph ^ 1 : qph;
         for (int t = 0; t < (two ? 2 : 1); ++t) {
-          const int k = 2 * r + t;
-          mbar_wait(q_full + k % nqb, (k / nqb) & 1);
+          PP_T0() mbar_wait(q_full + qb[t], qp[t]); PP_ADD(2)
         }
+        for (int u = 0; u < 2; ++u)
+          if (++qbuf == nqb) { qbuf = 0; qph ^= 1; }
         for (int j = 0; j < n; ++j) {
           int s = 0;
           for (int t = 0; t < (two ? 2 : 1); ++t) {
-            const int k = 2 * r + t;
             const uint32_t g = t ? step1 : step0;
             if (t) ++step1; else ++step0;
             const int buf = g & 1;
             // softmax of this slot is done reading S[buf] (step g - 2)
-            mbar_wait(s_free + 2 * t + buf, ((g >> 1) & 1) ^ 1);
+            { PP_T0() mbar_wait(s_free + 2 * t + buf, ((g >> 1) & 1) ^ 1); PP_ADD(0) }
             if (t == 0 || !shared) {
-              s = idx % nst;
-              mbar_wait(kv_full + s, (idx / nst) & 1);
-              ++idx;
+              s = ring_s;
+              { PP_T0() mbar_wait(kv_full + s, ring_ph); PP_ADD(1) }
+              if (++ring_s == nst) { ring_s = 0; ring_ph ^= 1; }
             }
             tc_fence_after();
-            const uint64_t da = dq0 + ((uint64_t)((k % nqb) * C::Q_BYTES) >> 4);
+            const uint64_t da = dq0 + ((uint64_t)(qb[t] * C::Q_BYTES) >> 4);
             const uint64_t db = dk0 + ((uint64_t)(s * C::STAGE_BYTES) >> 4);
+            {
+            PP_T0()
             if (leader) {
 #pragma unroll
               for (int kk = 0; kk < D / 16; ++kk) {
@@ -223,12 +330,21 @@ predict_kernel(const __grid_constant__ CUtensorMap tmap_q,
               }
               if (t == 1 || !shared || !two) mma_commit(kv_empty + s);
               mma_commit(s_full + 2 * t + buf);
-              if (j == n - 1) mma_commit(q_empty + k % nqb);
+              if (j == n - 1) mma_commit(q_empty + qb[t]);
+            }
+            PP_ADD(8)
+#ifdef SV_PRED_TRACE
+            if (TR_ON && leader && g < 400) {
+              sv_pred_tr_mma[t][g][0] = pp0_;
+              sv_pred_tr_mma[t][g][1] = clock64();
+            }
+#endif
             }
             __syncwarp();
           }
         }
       }
+      PP_ADD(5)
     }
     // no re-grow here: a loader that finished early would race the softmax warps' growth for
     // the CTA's register pool (setmaxnreg.inc blocks), and nothing after this needs registers
@@ -242,15 +358,25 @@ predict_kernel(const __grid_constant__ CUtensorMap tmap_q,
     const float sl2 = a.scale_log2;
     const uint64_t sl2x2 = f2_pack(sl2, sl2);
     float* my_sums = sums + t * n * BM;
-    float* my_part = part + t * C::NSEG * n;
     uint32_t g = 0;
+#ifdef SV_PRED_PROF
+    const long long ppk_ = clock64();
+#endif
     for (int k = t; k < T; k += 2) {
       const int it = lo + k;
       const int bh = it / n_tiles, tile = it % n_tiles;
       float m = -INFINITY;
+      float l = 0.f;   // running sum of the stored block sums (relative to m)
       for (int j = 0; j < n; ++j, ++g) {
         const int buf = g & 1;
-        mbar_wait(s_full + 2 * t + buf, (g >> 1) & 1);
+        { PP_T0() mbar_wait(s_full + 2 * t + buf, (g >> 1) & 1); if (quarter == 0) { PP_ADD(4) } else { PP_ADD(12) }
+#ifdef SV_PRED_TRACE
+          if (TR_ON && quarter == 0 && lane == 0 && g < 400) sv_pred_tr_sm[t][g][0] = pp0_;
+#endif
+        }
+#ifdef SV_PRED_PROF
+        const long long pps_ = clock64();
+#endif
         tc_fence_after();
         uint32_t sr[BLK];
         if constexpr (BLK >= 32) {
@@ -263,6 +389,18 @@ predict_kernel(const __grid_constant__ CUtensorMap tmap_q,
         tmem_wait_ld();
         tc_fence_before();
         mbar_arrive(s_free + 2 * t + buf);
+#ifdef SV_PRED_SKEL
+        if (true) {
+          my_sums[j * BM + row] = __uint_as_float(sr[0]) * 0.f + 1.f;
+#ifdef SV_PRED_TRACE
+          if (TR_ON && quarter == 0 && lane == 0 && g < 400) {
+            sv_pred_tr_sm[t][g][1] = pps_;
+            sv_pred_tr_sm[t][g][2] = clock64();
+          }
+#endif
+          continue;
+        }
+#endif
         const int valid = min(BLK, a.n_kv - j * BLK);   // ragged last KV block (READING 20)
         if (__builtin_expect(valid < BLK, 0)) {
 #pragma unroll
@@ -281,6 +419,7 @@ predict_kernel(const __grid_constant__ CUtensorMap tmap_q,
           // lazy rescale of the row's stored block sums (rare after the first blocks)
           const float alpha = ex2(m - mx_s);
           for (int jj = 0; jj < j; ++jj) my_sums[jj * BM + row] *= alpha;
+          l *= alpha;
           m = mx_s;
         }
         const uint64_t negm = f2_pack(-m, -m);
@@ -313,59 +452,68 @@ predict_kernel(const __grid_constant__ CUtensorMap tmap_q,
         float s0, s1;
         f2_unpack(s2, s0, s1);
         my_sums[j * BM + row] = s0 + s1;
+        l += s0 + s1;
+#ifdef SV_PRED_PROF
+        if (quarter == 0 && lane == 0) { PP_ATOMIC(6, clock64() - pps_) }
+#ifdef SV_PRED_TRACE
+        if (TR_ON && quarter == 0 && lane == 0 && g < 400) {
+          sv_pred_tr_sm[t][g][1] = pps_;
+          sv_pred_tr_sm[t][g][2] = clock64();
+        }
+#endif
+#endif
       }
+#ifdef SV_PRED_PROF
+      const long long ppe_ = clock64();
+#endif
       // ------------------------------------------------------------ tile end: masses
-      float l = 0.f;
-      for (int j = 0; j < n; ++j) l += my_sums[j * BM + row];
+      // P[q, j] = 2^(s' - m) / l: each row's normalised block sums, reduced over the warp's 32
+      // rows into part[t][pb][quarter][.] for the selection warp (double-buffered per slot)
       const bool row_valid = tile * BM + row < a.n_q;
       const float inv = row_valid ? 1.f / l : 0.f;
-      for (int j = 0; j < n; ++j) {
-        float w = my_sums[j * BM + row] * inv;
+      const int kk = k >> 1, pb = kk & 1;
+      float* pt = part + (t * 2 + pb) * C::NSEG * n;
+      if (kk >= 2) mbar_wait(part_free + 2 * t + pb, ((kk >> 1) - 1) & 1);
+      if constexpr (C::SEG == 32) {
+        // transpose-reduce: 31 shuffles per 32 blocks; lane i ends with the sum of block j0 + i
+        for (int j0 = 0; j0 < n; j0 += 32) {
+          float v[32];
 #pragma unroll
-        for (int off = C::SEG / 2; off > 0; off >>= 1) w += __shfl_xor_sync(0xffffffffu, w, off);
-        if ((lane % C::SEG) == 0) my_part[(row / C::SEG) * n + j] = w;
-      }
-      named_bar(1 + t, BM);
-      // selection: one warp per query block; the block's mass row is staged in my_sums
-      const int W = (n + 31) / 32;
-      constexpr int SEG_PER_G = BLK / C::SEG;
-      for (int gq = quarter; gq < C::G; gq += 4) {
-        const int u = tile * C::G + gq;
-        if (u >= a.g_q) continue;
-        float* mrow = my_sums + gq * n;
-        for (int v = lane; v < n; v += 32) {
-          float acc = 0.f;
-          for (int sgi = 0; sgi < SEG_PER_G; ++sgi) acc += my_part[(gq * SEG_PER_G + sgi) * n + v];
-          mrow[v] = acc;
-        }
-        __syncwarp();
-        const long long r = (long long)bh * a.g_q + u;
-        const int rows_u = min(BLK, a.n_q - u * BLK);
-        const float thr = a.tau * float(rows_u);
-        for (int w0 = 0; w0 < W; ++w0) {
-          const int v = w0 * 32 + lane;
-          bool sel = false;
-          if (v < n) {
-            const float mv = mrow[v];
-            if (a.mode == 0) {
-              int rank = 0;
-              for (int tt = 0; tt < n; ++tt) {
-                const float mt = mrow[tt];
-                rank += (mt > mv) || (mt == mv && tt < v);
-              }
-              sel = rank < a.topk;
-            } else {
-              sel = mv >= thr;
+          for (int i = 0; i < 32; ++i) v[i] = j0 + i < n ? my_sums[(j0 + i) * BM + row] * inv : 0.f;
+#pragma unroll
+          for (int sh = 16; sh >= 1; sh >>= 1) {
+            const bool up = (lane & sh) != 0;
+#pragma unroll
+            for (int i = 0; i < sh; ++i) {
+              const float send = up ? v[i] : v[i + sh];
+              const float keep = up ? v[i + sh] : v[i];
+              v[i] = keep + __shfl_xor_sync(0xffffffffu, send, sh);
             }
-            sel = sel || (v < a.n_sink_blocks);
-            if (a.mass) a.mass[r * n + v] = mv;
           }
-          const uint32_t word = __ballot_sync(0xffffffffu, sel);
-          if (lane == 0) a.mask[r * W + w0] = word;
+          if (j0 + lane < n) pt[quarter * n + j0 + lane] = v[0];
+        }
+      } else {
+        for (int j = 0; j < n; ++j) {
+          float w = my_sums[j * BM + row] * inv;
+#pragma unroll
+          for (int off = C::SEG / 2; off > 0; off >>= 1) w += __shfl_xor_sync(0xffffffffu, w, off);
+          if ((lane % C::SEG) == 0) pt[(row / C::SEG) * n + j] = w;
         }
       }
-      named_bar(1 + t, BM);   // my_sums / my_part are reused by the next tile
+      mbar_arrive(part_full + 2 * t + pb);
+#ifdef SV_PRED_PROF
+      if (quarter == 0 && lane == 0) { PP_ATOMIC(7, clock64() - ppe_) }
+#ifdef SV_PRED_TRACE
+      if (TR_ON && quarter == 0 && lane == 0 && (k >> 1) < 16) {
+        sv_pred_tr_te[t][k >> 1][0] = ppe_;
+        sv_pred_tr_te[t][k >> 1][1] = clock64();
+      }
+#endif
+#endif
     }
+#ifdef SV_PRED_PROF
+    if (quarter == 0 && lane == 0) { PP_ATOMIC(9, clock64() - ppk_) }
+#endif
     reg_dealloc<REG_LAUNCH>();
   }
 

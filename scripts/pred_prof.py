@@ -1,5 +1,4 @@
-"""Development aid: blocked-clock breakdown of the column-split predictor (SV_PRED_PROF build of
-experiments/predictor_column_split.cu.txt copied over csrc/predictor.cu).
+"""Development aid: blocked-clock breakdown of the predictor roles (-DSV_PRED_PROF build).
     SPARVAR_LIB=variants/lib_pprof.so python scripts/pred_prof.py"""
 import ctypes
 import os
@@ -20,15 +19,16 @@ for _ in range(reps):
     fn()
 torch.cuda.synchronize()
 buf = (ctypes.c_ulonglong * 16)()
+sv.lib.sparvar_pred_prof_read.argtypes = [ctypes.c_void_p]
 sv.lib.sparvar_pred_prof_read(buf)
 ncta = 148 * reps
 names = {0: "MMA wait s_free", 1: "MMA wait kv_full", 2: "MMA wait q_full", 3: "K loader wait kv_empty",
-         4: "softmax(q0 warps) wait s_full", 5: "MMA loop total", 6: "softmax(q0 warps) loop total",
-         7: "softmax(q0 warps) tile-end", 12: "softmax(other warps) wait s_full", 8: "MMA issue of 8 tcgen05.mma (leader)"}
+         4: "softmax(q0 warps) wait s_full", 5: "MMA loop total", 6: "softmax(q0) step bodies",
+         7: "softmax(q0 warps) tile-end", 9: "softmax(q0) whole", 12: "softmax(other warps) wait s_full", 8: "MMA issue of 8 tcgen05.mma (leader)"}
 for i, n in names.items():
     per = buf[i] / ncta
-    if i in (4, 6, 7):
-        per /= 4      # four quarter-0 warps per CTA
+    if i in (4, 6, 7, 9):
+        per /= 2      # the two quarter-0 softmax warps per CTA (one per slot)
     if i == 12:
-        per /= 12
+        per /= 6      # the other six softmax warps
     print(f"{n:36s} {per:12.0f} clk per CTA-launch")
