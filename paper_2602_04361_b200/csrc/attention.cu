@@ -43,19 +43,23 @@
 
 #ifdef SV_PROF
 // Development instrumentation (variant libraries only, scripts/build_variant.sh).
-__device__ long long sv_prof_buf[8192];
+__device__ long long sv_prof_buf[24576];
 extern "C" int sparvar_prof_read(long long* host, int n) {
   return cudaMemcpyFromSymbol(host, sv_prof_buf, sizeof(long long) * n) == cudaSuccess ? 0 : 1;
 }
 #define SV_STAMP(i_) \
-  if (blockIdx.x == 0 && threadIdx.x == 0 && (i_) < 5000) sv_prof_buf[(i_)] = clock64();
+  if (blockIdx.x == 0 && (threadIdx.x & 127) == 0 && threadIdx.x < 256 && (i_) < 2500) \
+    sv_prof_buf[(i_) + (threadIdx.x >> 7) * 2500] = clock64();
 #define SV_STAMP_CTA(base_) \
   if (threadIdx.x == 0 && blockIdx.x < 192) sv_prof_buf[(base_) + blockIdx.x] = (long long)globaltimer_ns();
 #define SV_ACC(base_, v_) \
   if (blockIdx.x < 192) atomicAdd((unsigned long long*)&sv_prof_buf[(base_) + blockIdx.x], (unsigned long long)(v_));
 #define SV_CLK() clock64()
+// MMA issuer op trace of CTA 0: [8192 + 4 * op + {0: before P wait, 1: after, 2: PV issued, 3: QK issued}]
+#define SV_OPSTAMP(op_, k_) \
+  if (blockIdx.x == 0 && lane == 0 && (op_) < 1000) sv_prof_buf[8192 + 8 * (op_) + (k_)] = clock64();
 extern "C" int sparvar_prof_reset() {
-  static long long z[8192];
+  static long long z[24576];
   return cudaMemcpyToSymbol(sv_prof_buf, z, sizeof(z)) == cudaSuccess ? 0 : 1;
 }
 #else
@@ -63,6 +67,7 @@ extern "C" int sparvar_prof_reset() {
 #define SV_STAMP_CTA(base_) {}
 #define SV_ACC(base_, v_) {}
 #define SV_CLK() 0LL
+#define SV_OPSTAMP(op_, k_) {}
 #endif
 
 #ifndef SV_EMU_EVERY
@@ -572,6 +577,12 @@ attn_fwd_kernel(const __grid_constant__ CUtensorMap tmap_q,
               const long long t0_ = SV_CLK();
               mbar_wait(kv_empty + s, ph ^ 1);
               SV_ACC(5000, SV_CLK() - t0_)
+#ifdef SV_PROF
+              if (blockIdx.x == 0 && kv_idx <= 2000) {
+                sv_prof_buf[16384 + 2 * (kv_idx - 1)] = t0_;
+                sv_prof_buf[16384 + 2 * (kv_idx - 1) + 1] = clock64();
+              }
+#endif
             }
             uint8_t* dst = sKV + s * C::STAGE_BYTES;
             mbar_arrive_expect_tx(kv_full + s, C::STAGE_BYTES);
@@ -681,6 +692,9 @@ attn_fwd_kernel(const __grid_constant__ CUtensorMap tmap_q,
         auto next_stage = [&]() -> uint32_t {
           const int s = ring_s;
           SV_MMA_WAIT_T(kv_full + s, ring_ph, 6000);
+#ifdef SV_PROF
+          if (blockIdx.x == 0 && lane == 0 && kv_idx < 2000) sv_prof_buf[20480 + kv_idx] = clock64();
+#endif
           if (++ring_s == C::NST) { ring_s = 0; ring_ph ^= 1; }
           ++kv_idx;
           return (uint32_t)s;
@@ -729,9 +743,18 @@ attn_fwd_kernel(const __grid_constant__ CUtensorMap tmap_q,
             const int jn = t ? jn1 : jn0, nn = t ? nn1 : nn0, qb = t ? qb1 : qb0;
             const int tdone = t ? tiles1 : tiles0;
             // the stages this op reads are (normally) resident already: check them before P
+#ifdef SV_PROF
+            SV_OPSTAMP((int)(p_cnt0 + p_cnt1), 4)
+#endif
             const uint32_t sv = next_stage();
+#ifdef SV_PROF
+            SV_OPSTAMP((int)(p_cnt0 + p_cnt1), 5)
+#endif
             const bool more = jn + 1 < nn;
             const uint32_t sk = more ? next_stage() : 0u;
+#ifdef SV_PROF
+            SV_OPSTAMP((int)(p_cnt0 + p_cnt1), 6)
+#endif
             const uint32_t par = (t ? p_cnt1 : p_cnt0) & 1;
             if (t) ++p_cnt1; else ++p_cnt0;
             if (lane == 0) SV_ACC(7000, 1)
@@ -740,11 +763,18 @@ attn_fwd_kernel(const __grid_constant__ CUtensorMap tmap_q,
             const uint32_t p_tmem = tmem + t * 128;
             // the tile's first P.V overwrites O: the epilogue must have drained the previous one
             if (jn == 0 && tdone > 0) SV_MMA_WAIT_T(o_free + t, (tdone - 1) & 1, 6400);
+#ifdef SV_PROF
+            const int op_ = (int)(p_cnt0 + p_cnt1) - 1;
+            SV_OPSTAMP(op_, 0)
+#endif
 #if SV_LEAN
             // O_t += P_t V_j: every softmax thread arrives on the first-half barrier before the
             // second, so waiting on the second covers all of P (one wait + fence per op: the
             // issue queue is shallow, every instruction here is tensor-pipe idle time)
             SV_MMA_WAIT_T(p_bar + 2 * t + 1, par, 6200);
+#ifdef SV_PROF
+            SV_OPSTAMP(op_, 1)
+#endif
             tc_fence_after();
             if (leader) {
 #pragma unroll
@@ -753,6 +783,9 @@ attn_fwd_kernel(const __grid_constant__ CUtensorMap tmap_q,
                        (jn > 0 || kk > 0) ? 1u : 0u);
               mma_commit(kv_empty + sv);
             }
+#ifdef SV_PROF
+            SV_OPSTAMP(op_, 2)
+#endif
 #else
             // O_t += P_t V_j in two halves: the first as soon as half of P is in TMEM
             SV_MMA_WAIT(p_bar + 2 * t, par);
@@ -777,6 +810,9 @@ attn_fwd_kernel(const __grid_constant__ CUtensorMap tmap_q,
             if (more) {
               if (t) ++jn1; else ++jn0;
               issue_qk(t, sk, qb, jn + 2 == nn);
+#ifdef SV_PROF
+              SV_OPSTAMP(op_, 3)
+#endif
             } else {
               if (leader) mma_commit(o_bar + t);
               __syncwarp();

@@ -17,7 +17,7 @@
 //    than 2^8).  At the tile end each row normalises by l = sum of its block sums (exact:
 //    P[q, j] = 2^(s' - m) / l), rows are reduced per query block in a fixed order
 //    (deterministic), and one warp per query block selects with ballots into bit rows.
-//  * One in eight exp2 pairs runs as a degree-4 polynomial on the FMA pipe (relative error
+//  * One in four exp2 pairs runs as a degree-4 polynomial on the FMA pipe (relative error
 //    2.6e-6, well inside the 1e-4 mass tolerance) to take load off the MUFU pipe.
 #include <cuda_bf16.h>
 #include <cstdio>
@@ -30,8 +30,11 @@
 #ifndef SV_PRED_QB
 #define SV_PRED_QB 4     // preferred number of Q buffers (2..4); fewer if shared memory is short
 #endif
+#ifndef SV_PRED_ORDER
+#define SV_PRED_ORDER 0   // 0: contiguous tile ranges; 1: same-head tile pairs in strided windows
+#endif
 #ifndef SV_PRED_EMU_EVERY
-#define SV_PRED_EMU_EVERY 8   // 1 in 8 exp2 pairs as a degree-4 polynomial on the FMA pipe
+#define SV_PRED_EMU_EVERY 4   // 1 in 4 exp2 pairs as a degree-4 polynomial on the FMA pipe
 #endif
 
 #ifdef SV_PRED_PROF
@@ -71,6 +74,11 @@ extern "C" int sparvar_pred_trace_read(long long* sm, long long* mma, long long*
 
 namespace sv {
 namespace {
+
+__host__ __device__ inline int gcd_pred(int a, int b) {
+  while (b) { const int t = a % b; a = b; b = t; }
+  return a;
+}
 
 constexpr int BM = 128;
 constexpr int NUM_WARPS = 12;   // WG0/WG1 softmax slot 0/1, warp 8 MMA, 9 K, 10 Q, 11 selection
@@ -143,10 +151,44 @@ predict_kernel(const __grid_constant__ CUtensorMap tmap_q,
   const int lane = threadIdx.x & 31;
   const int n_tiles = (a.n_q + BM - 1) / BM;
   const int items = n_tiles * a.bh;
+#if SV_PRED_ORDER == 0
   // contiguous, equal-size range of tiles (every tile costs the same n steps)
   const int lo = (int)((long long)items * blockIdx.x / gridDim.x);
   const int hi = (int)((long long)items * (blockIdx.x + 1) / gridDim.x);
   const int T = hi - lo;
+  // global tile (head * n_tiles + tile) of slot use k (slot k & 1, round k >> 1), or -1
+  auto tile_of = [&](int k) -> int { return k < T ? lo + k : -1; };
+#else
+  // Rounds of two tiles (one per slot).  FULL rounds take pairs of adjacent tiles of one (b,h)
+  // (both slots share every K stage), dealt in strided windows: round r of CTA c takes pair
+  // r * grid + (c + rot * r) mod grid, so the grid works on ~grid consecutive pairs at a time (a
+  // few heads, their K_{<=S} L2-resident).  For an odd tile count the last tile of every head is
+  // a SINGLE round (slot 1 idle), dealt one per CTA starting with the CTAs that have one full
+  // round fewer.
+  (void)items;
+  const int fp = n_tiles / 2;
+  const int n_full = fp * a.bh;
+  const int n_single = (n_tiles & 1) ? a.bh : 0;
+  const int grid = gridDim.x;
+  int rot = 59;
+  while (grid > 1 && gcd_pred(rot % grid, grid) != 1) rot += 2;
+  const int k_full = n_full / grid, rem = n_full - k_full * grid;
+  const int pos = (int)((blockIdx.x + (long long)k_full * rot) % grid);
+  const int mine_full = k_full + (pos < rem ? 1 : 0);
+  const int s_first = (pos - rem + grid) % grid;
+  const int mine_single = s_first < n_single ? (n_single - s_first + grid - 1) / grid : 0;
+  const int T = 2 * (mine_full + mine_single);
+  auto tile_of = [&](int k) -> int {
+    const int r = k >> 1, t = k & 1;
+    if (r < mine_full) {
+      const int pr = r * grid + (int)((blockIdx.x + (long long)r * rot) % grid);
+      return (pr / fp) * n_tiles + 2 * (pr % fp) + t;
+    }
+    if (t == 1 || r - mine_full >= mine_single) return -1;
+    const int sg = s_first + (r - mine_full) * grid;
+    return sg * n_tiles + n_tiles - 1;
+  };
+#endif
 
   if (threadIdx.x == 0) {
     if ((smem_u32(smem) & 1023u) != 0) {
@@ -179,18 +221,22 @@ predict_kernel(const __grid_constant__ CUtensorMap tmap_q,
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
-  // tile k of this CTA (item lo + k) runs in slot k & 1, round k >> 1; Q buffer k % nqb.
-  // Both slots of a round start and end together (equal step counts).
+  // slot use k (tile tile_of(k)) runs in slot k & 1, round k >> 1; the valid uses take the Q
+  // buffers in order (the q-th valid one buffer q % nqb).  Both slots of a round start and end
+  // together (equal step counts); a round without slot 1 has tile_of(2r + 1) < 0.
 
   if (warp >= 8) {
     reg_dealloc<REG_OTHER>();
     if (warp == WARP_Q) {
       // ---------------------------------------------------------------- Q loader
       if (lane == 0) {
+        int q = 0;
         for (int k = 0; k < T; ++k) {
-          const int b = k % nqb;
-          if (k >= nqb) mbar_wait(q_empty + b, ((k / nqb) - 1) & 1);
-          const int it = lo + k;
+          const int it = tile_of(k);
+          if (it < 0) continue;
+          const int b = q % nqb;
+          if (q >= nqb) mbar_wait(q_empty + b, ((q / nqb) - 1) & 1);
+          ++q;
           mbar_arrive_expect_tx(q_full + b, C::Q_BYTES);
 #pragma unroll
           for (int x = 0; x < C::NBOX; ++x)
@@ -204,12 +250,13 @@ predict_kernel(const __grid_constant__ CUtensorMap tmap_q,
         const uint64_t pol = policy_evict_last();
         int idx = 0;
         for (int r = 0; 2 * r < T; ++r) {
-          const int bh0 = (lo + 2 * r) / n_tiles;
-          const bool two = 2 * r + 1 < T;
-          const bool shared = two && (lo + 2 * r + 1) / n_tiles == bh0;
+          const int it0 = tile_of(2 * r), it1 = tile_of(2 * r + 1);
+          const int bh0 = it0 / n_tiles;
+          const bool two = it1 >= 0;
+          const bool shared = two && it1 / n_tiles == bh0;
           for (int j = 0; j < n; ++j) {
             for (int t = 0; t < (two && !shared ? 2 : 1); ++t) {
-              const int bh = (lo + 2 * r + t) / n_tiles;
+              const int bh = (t ? it1 : it0) / n_tiles;
               const int s = idx % nst;
               const uint32_t ph = (idx / nst) & 1;
               ++idx;
@@ -233,8 +280,9 @@ predict_kernel(const __grid_constant__ CUtensorMap tmap_q,
       for (int k = 0; k < T; ++k) {
         const int t = k & 1, kk = k >> 1, pb = kk & 1;
         const float* pt = part + (t * 2 + pb) * C::NSEG * n;
+        const int it = tile_of(k);
+        if (it < 0) continue;
         mbar_wait(part_full + 2 * t + pb, (kk >> 1) & 1);
-        const int it = lo + k;
         const int bh = it / n_tiles, tile = it % n_tiles;
         for (int gq = 0; gq < C::G; ++gq) {
           const int u = tile * C::G + gq;
@@ -289,9 +337,10 @@ predict_kernel(const __grid_constant__ CUtensorMap tmap_q,
       uint32_t step0 = 0, step1 = 0;   // S buffer uses per slot
       PP_T0()
       for (int r = 0; 2 * r < T; ++r) {
-        const bool two = 2 * r + 1 < T;
-        const bool shared = two && (lo + 2 * r + 1) / n_tiles == (lo + 2 * r) / n_tiles;
-        // Q buffers of the round's tiles (use k = 2r + t: buffer k % nqb, parity (k / nqb) & 1)
+        const int it0 = tile_of(2 * r), it1 = tile_of(2 * r + 1);
+        const bool two = it1 >= 0;
+        const bool shared = two && it1 / n_tiles == it0 / n_tiles;
+        // Q buffers of the round's tiles (the q-th valid use: buffer q % nqb, parity (q / nqb) & 1)
         int qb[2];
         uint32_t qp[2];
         qb[0] = qbuf;
@@ -301,7 +350,7 @@ predict_kernel(const __grid_constant__ CUtensorMap tmap_q,
         for (int t = 0; t < (two ? 2 : 1); ++t) {
           PP_T0() mbar_wait(q_full + qb[t], qp[t]); PP_ADD(2)
         }
-        for (int u = 0; u < 2; ++u)
+        for (int u = 0; u < (two ? 2 : 1); ++u)
           if (++qbuf == nqb) { qbuf = 0; qph ^= 1; }
         for (int j = 0; j < n; ++j) {
           int s = 0;
@@ -363,13 +412,16 @@ predict_kernel(const __grid_constant__ CUtensorMap tmap_q,
     const long long ppk_ = clock64();
 #endif
     for (int k = t; k < T; k += 2) {
-      const int it = lo + k;
-      const int bh = it / n_tiles, tile = it % n_tiles;
+      const int it = tile_of(k);
+      if (it < 0) continue;
+      const int tile = it % n_tiles;
       float m = -INFINITY;
       float l = 0.f;   // running sum of the stored block sums (relative to m)
       for (int j = 0; j < n; ++j, ++g) {
         const int buf = g & 1;
-        { PP_T0() mbar_wait(s_full + 2 * t + buf, (g >> 1) & 1); if (quarter == 0) { PP_ADD(4) } else { PP_ADD(12) }
+        { PP_T0()
+          mbar_wait(s_full + 2 * t + buf, (g >> 1) & 1);
+          if (quarter == 0) { PP_ADD(4) } else { PP_ADD(12) }
 #ifdef SV_PRED_TRACE
           if (TR_ON && quarter == 0 && lane == 0 && g < 400) sv_pred_tr_sm[t][g][0] = pp0_;
 #endif
@@ -389,18 +441,6 @@ predict_kernel(const __grid_constant__ CUtensorMap tmap_q,
         tmem_wait_ld();
         tc_fence_before();
         mbar_arrive(s_free + 2 * t + buf);
-#ifdef SV_PRED_SKEL
-        if (true) {
-          my_sums[j * BM + row] = __uint_as_float(sr[0]) * 0.f + 1.f;
-#ifdef SV_PRED_TRACE
-          if (TR_ON && quarter == 0 && lane == 0 && g < 400) {
-            sv_pred_tr_sm[t][g][1] = pps_;
-            sv_pred_tr_sm[t][g][2] = clock64();
-          }
-#endif
-          continue;
-        }
-#endif
         const int valid = min(BLK, a.n_kv - j * BLK);   // ragged last KV block (READING 20)
         if (__builtin_expect(valid < BLK, 0)) {
 #pragma unroll
@@ -547,7 +587,11 @@ cudaError_t launch_t(const CUtensorMap& tq, const CUtensorMap& tk, const PredArg
   auto kern = predict_kernel<D, BLK>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
+#if SV_PRED_ORDER == 0
   const long long items = (long long)((a.n_q + BM - 1) / BM) * a.bh;
+#else
+  const long long items = 2 * (((long long)((a.n_q + BM - 1) / BM) * a.bh + 1) / 2);
+#endif
   if (items <= 0) return cudaSuccess;
   const int sms = num_sms_pred();
   const int grid = (int)(items >= 2LL * sms ? sms : (items + 1) / 2);

@@ -21,9 +21,10 @@ mma = (ctypes.c_longlong * (2 * 400 * 2))()
 te = (ctypes.c_longlong * (2 * 16 * 2))()
 sv.lib.sparvar_pred_trace_read.argtypes = [ctypes.c_void_p] * 3
 assert sv.lib.sparvar_pred_trace_read(sm, mma, te) == 0
-done = (ctypes.c_longlong * (2 * 400))()
-sv.lib.sparvar_pred_trace_done.argtypes = [ctypes.c_void_p]
-assert sv.lib.sparvar_pred_trace_done(done) == 0
+done = (ctypes.c_longlong * (2 * 400))()   # S completion times, when the build records them
+if hasattr(sv.lib, "sparvar_pred_trace_done"):
+    sv.lib.sparvar_pred_trace_done.argtypes = [ctypes.c_void_p]
+    assert sv.lib.sparvar_pred_trace_done(done) == 0
 DN = lambda t, g: done[t * 400 + g]  # noqa: E731
 SM = lambda t, g, i: sm[(t * 400 + g) * 3 + i]  # noqa: E731
 MM = lambda t, g, i: mma[(t * 400 + g) * 2 + i]  # noqa: E731

@@ -25,9 +25,9 @@ torch.cuda.synchronize()
 sv.lib.sparvar_prof_reset()
 fn()
 torch.cuda.synchronize()
-buf = (ctypes.c_longlong * 8192)()
+buf = (ctypes.c_longlong * 24576)()
 sv.lib.sparvar_prof_read.argtypes = [ctypes.c_void_p, ctypes.c_int]
-sv.lib.sparvar_prof_read(buf, 8192)
+sv.lib.sparvar_prof_read(buf, 24576)
 a = np.array(buf[:], dtype=np.int64)
 n = int((a != 0).sum() // 5)
 st = a[:5 * n].reshape(n, 5)
