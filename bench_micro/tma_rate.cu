@@ -4,6 +4,7 @@
 //   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -I paper_2602_04361_b200/csrc \
 //        bench_micro/tma_rate.cu -o bench_micro/tma_rate -lcuda
 #include <cstdio>
+#include <cstdlib>
 #include <cuda.h>
 #include "ptx.cuh"
 using namespace sv;
@@ -24,7 +25,7 @@ __global__ void __launch_bounds__(64, 1) k_tma(const __grid_constant__ CUtensorM
       const int s = i % NST;
       if (i >= NST) mbar_wait(full + s, ((i / NST) - 1) & 1);
       if (i < iters) {
-        const int row = ((blockIdx.x * 7 + i) * 128) % rows_total;
+        const int row = (int)((((long long)blockIdx.x * 7919 + (long long)i * 148) * 128) % rows_total);
         mbar_arrive_expect_tx(full + s, 32768);
         tma_load_3d(sm + s * 32768, &tm, full + s, 0, row, 0);
         tma_load_3d(sm + s * 32768 + 16384, &tm, full + s, 64, row, 0);
@@ -38,8 +39,10 @@ typedef CUresult (*EncodeFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void
                              const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
                              CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
 
-int main() {
-  const int rows = 8192 * 4;   // 8 MB of bf16 x 128: L2-resident
+int main(int argc, char** argv) {
+  // default 8 MB of bf16 x 128 (L2-resident); argv[1] = MB for a DRAM-resident buffer
+  const int mb = argc > 1 ? atoi(argv[1]) : 8;
+  const int rows = mb * 4096;
   void* buf;
   cudaMalloc(&buf, (size_t)rows * 128 * 2);
   cudaMemset(buf, 0, (size_t)rows * 128 * 2);

@@ -52,8 +52,12 @@ extern "C" int sparvar_prof_read(long long* host, int n) {
     sv_prof_buf[(i_) + (threadIdx.x >> 7) * 2500] = clock64();
 #define SV_STAMP_CTA(base_) \
   if (threadIdx.x == 0 && blockIdx.x < 192) sv_prof_buf[(base_) + blockIdx.x] = (long long)globaltimer_ns();
+#ifdef SV_PROF_LITE   // timeline stamps only: no per-wait atomics
+#define SV_ACC(base_, v_) {}
+#else
 #define SV_ACC(base_, v_) \
   if (blockIdx.x < 192) atomicAdd((unsigned long long*)&sv_prof_buf[(base_) + blockIdx.x], (unsigned long long)(v_));
+#endif
 #define SV_CLK() clock64()
 // MMA issuer op trace of CTA 0: [8192 + 4 * op + {0: before P wait, 1: after, 2: PV issued, 3: QK issued}]
 #define SV_OPSTAMP(op_, k_) \
@@ -727,10 +731,23 @@ attn_fwd_kernel(const __grid_constant__ CUtensorMap tmap_q,
           const int qb = (meta >> 1) & 3;
           const int n = sm->n[ic];
           if (t) { qb1 = qb; nn1 = n; jn1 = 0; } else { qb0 = qb; nn0 = n; jn0 = 0; }
+#ifdef SV_PROF
+          const int st_ = tiles0 + tiles1;
+          if (blockIdx.x == 0 && lane == 0 && st_ < 500) sv_prof_buf[22528 + 4 * st_] = clock64();
+#endif
           const uint32_t s = next_stage();
+#ifdef SV_PROF
+          if (blockIdx.x == 0 && lane == 0 && st_ < 500) sv_prof_buf[22528 + 4 * st_ + 1] = clock64();
+#endif
           SV_MMA_WAIT_T(q_full + qb, (meta >> 3) & 1, 6600);
+#ifdef SV_PROF
+          if (blockIdx.x == 0 && lane == 0 && st_ < 500) sv_prof_buf[22528 + 4 * st_ + 2] = clock64();
+#endif
           tc_fence_after();
           issue_qk(t, s, qb, n == 1);
+#ifdef SV_PROF
+          if (blockIdx.x == 0 && lane == 0 && st_ < 500) sv_prof_buf[22528 + 4 * st_ + 3] = clock64();
+#endif
         };
         const long long tm0_ = SV_CLK();
         start(0, 0);

@@ -88,3 +88,18 @@ if n > 50:
     print("stage 100..110 rel: [loader wait start, issue, issuer sees full]")
     for i in range(100, 110):
         print(i, int(ld[i, 0] - t0), int(ld[i, 1] - t0), int(use[i] - t0))
+# issuer tile starts of CTA 0: [enter, K stage ready, Q ready, QK issued]
+ts = a[22528:22528 + 2000].reshape(500, 4)
+ts = ts[ts[:, 0] > 0]
+if len(ts):
+    m = lambda x: float(np.median(x))  # noqa: E731
+    print(f"tile starts {len(ts)}: K-stage wait {m(ts[:, 1] - ts[:, 0]):.0f} (max {int((ts[:, 1] - ts[:, 0]).max())})  "
+          f"Q wait {m(ts[:, 2] - ts[:, 1]):.0f} (max {int((ts[:, 2] - ts[:, 1]).max())})  QK issue {m(ts[:, 3] - ts[:, 2]):.0f}")
+# step-period outliers per slot: how much time the long periods (tile boundaries) add
+for t, x in enumerate(sl):
+    per = np.diff(x[:, 1])
+    med = np.median(per)
+    big = per[per > 1.4 * med]
+    print(f"slot {t}: periods median {med:.0f} p90 {np.percentile(per, 90):.0f} max {per.max()}; "
+          f"{len(big)} long periods add {int((big - med).sum())} clk of {int(per.sum())} "
+          f"({100 * (big - med).sum() / per.sum():.1f}%)")
