@@ -7,16 +7,20 @@
 //     keep TOPK(k) (ties to the smaller v) or mass >= tau * |u|, then OR the sink blocks.
 //
 // Design (DESIGN.md §7 "predict_kernel"):
-//  * Persistent, one CTA per SM, two tile SLOTS (128 query rows each) with their own softmax
-//    warpgroup and a double-buffered S in TMEM (4 x 128 columns): the tensor core computes
-//    S_{j+1} while the softmax warps reduce S_j, so the kernel runs at the exp2 throughput.
-//  * Every tile has the same G_kvS KV steps, so the MMA warp and the K loader alternate the two
-//    slots in lockstep; when both slots work on the same (b,h) they share each K stage.
-//  * Per (row, KV block) the softmax warps keep the block sum of 2^(s*scale*log2e - m) relative
-//    to the row's running max m (lazy: the stored sums are rescaled only when m grows by more
-//    than 2^8).  At the tile end each row normalises by l = sum of its block sums (exact:
-//    P[q, j] = 2^(s' - m) / l), rows are reduced per query block in a fixed order
-//    (deterministic), and one warp per query block selects with ballots into bit rows.
+//  * Persistent, one CTA per SM, NS tile SLOTS of 128 query rows, each with its own softmax
+//    warpgroup and its own S accumulator in TMEM.  NS = 3 where shared memory allows it (three
+//    softmax warps per SM sub-partition keep the MUFU pipe busier than two), else NS = 2 with a
+//    double-buffered S per slot.  The tensor core computes a slot's next S while its softmax
+//    reduces the current one (the softmax releases S as soon as its last TMEM load lands).
+//  * Every tile has the same G_kvS KV steps, so the MMA warp and the K loader run the slots of a
+//    round in lockstep; slots of a round on the same (b,h) share each K stage.
+//  * Per (row, KV block) the softmax keeps the block sum of 2^(s*scale*log2e - m) relative to
+//    the row's running max m (lazy: rescaled only when m grows by more than 2^8) and the row
+//    total l in a register.  With NS = 3 a 128-key step is read from TMEM in two 64-column
+//    chunks twice (max pass, then exp2 pass) to fit 152 registers per thread.  At the tile end
+//    the rows are normalised by 1/l (exact: P[q, j] = 2^(s' - m) / l) and reduced per KV block
+//    with a transpose-reduce into a partial-mass buffer; a selection warp sums the partials in a
+//    fixed order (deterministic) and selects with ballots into bit rows.
 //  * One in four exp2 pairs runs as a degree-4 polynomial on the FMA pipe (relative error
 //    2.6e-6, well inside the 1e-4 mass tolerance) to take load off the MUFU pipe.
 #include <cuda_bf16.h>
@@ -27,76 +31,41 @@
 #include "ptx.cuh"
 #include "kernel_util.cuh"
 
-#ifndef SV_PRED_QB
-#define SV_PRED_QB 4     // preferred number of Q buffers (2..4); fewer if shared memory is short
-#endif
-#ifndef SV_PRED_ORDER
-#define SV_PRED_ORDER 0   // 0: contiguous tile ranges; 1: same-head tile pairs in strided windows
-#endif
 #ifndef SV_PRED_EMU_EVERY
 #define SV_PRED_EMU_EVERY 4   // 1 in 4 exp2 pairs as a degree-4 polynomial on the FMA pipe
 #endif
-
-#ifdef SV_PRED_PROF
-// Development instrumentation (variant libraries only, -DSV_PRED_PROF): clocks summed over CTAs.
-__device__ unsigned long long sv_pred_prof[16];
-extern "C" int sparvar_pred_prof_read(unsigned long long* host) {
-  return cudaMemcpyFromSymbol(host, sv_pred_prof, sizeof(sv_pred_prof)) == cudaSuccess ? 0 : 1;
-}
-extern "C" int sparvar_pred_prof_reset() {
-  static unsigned long long z[16];
-  return cudaMemcpyToSymbol(sv_pred_prof, z, sizeof(z)) == cudaSuccess ? 0 : 1;
-}
-#ifdef SV_PRED_TRACE
-// one CTA's timeline: softmax (quarter-0 warp of each slot) wait/body/end per step, the issuer's
-// MMA block per slot-step, tile ends
-__device__ long long sv_pred_tr_sm[2][400][3];
-__device__ long long sv_pred_tr_mma[2][400][2];
-__device__ long long sv_pred_tr_te[2][16][2];
-extern "C" int sparvar_pred_trace_read(long long* sm, long long* mma, long long* te) {
-  return (cudaMemcpyFromSymbol(sm, sv_pred_tr_sm, sizeof(sv_pred_tr_sm)) == cudaSuccess &&
-          cudaMemcpyFromSymbol(mma, sv_pred_tr_mma, sizeof(sv_pred_tr_mma)) == cudaSuccess &&
-          cudaMemcpyFromSymbol(te, sv_pred_tr_te, sizeof(sv_pred_tr_te)) == cudaSuccess) ? 0 : 1;
-}
-#define TR_ON (blockIdx.x == SV_PRED_TRACE)
-#endif
-#define PP_T0() const long long pp0_ = clock64();
-#ifdef SV_PRED_TRACE_ONLY
-#define PP_ATOMIC(i_, v_)
-#else
-#define PP_ATOMIC(i_, v_) atomicAdd(&sv_pred_prof[i_], (unsigned long long)(v_));
-#endif
-#define PP_ADD(i_) if ((threadIdx.x & 31) == 0) { PP_ATOMIC(i_, clock64() - pp0_) }
-#else
-#define PP_T0()
-#define PP_ADD(i_)
+#ifndef SV_PRED_MAX_SLOTS
+#define SV_PRED_MAX_SLOTS 3   // 3: use three slots when shared memory allows, 2: always two
 #endif
 
 namespace sv {
 namespace {
 
-__host__ __device__ inline int gcd_pred(int a, int b) {
-  while (b) { const int t = a % b; a = b; b = t; }
-  return a;
-}
-
 constexpr int BM = 128;
-constexpr int NUM_WARPS = 12;   // WG0/WG1 softmax slot 0/1, warp 8 MMA, 9 K, 10 Q, 11 selection
-constexpr int NUM_THREADS = NUM_WARPS * 32;
-constexpr int WARP_MMA = 8, WARP_K = 9, WARP_Q = 10, WARP_SEL = 11;
-constexpr int REG_LAUNCH = 168;
-constexpr int REG_SOFTMAX = 208;
-constexpr int REG_OTHER = 88;
-static_assert(8 * (REG_SOFTMAX - REG_LAUNCH) <= 4 * (REG_LAUNCH - REG_OTHER), "register pool");
 constexpr uint32_t TMEM_COLS = 512;
 constexpr int EMU_EVERY = SV_PRED_EMU_EVERY;
 constexpr int SMEM_LIMIT = 232448;
-constexpr int MAXQ = 4;
-// q full/empty, kv full/empty, s full/free [2][2], part full/free [2][2]
-constexpr int NBARS = 2 * MAXQ + 2 * 8 + 8 + 8;
+constexpr int MAXQ = 6;
+// q full/empty [MAXQ], kv full/empty [8], s full/free [NS * NB <= 4], part full/free [NS][2]
+constexpr int NBARS = 2 * MAXQ + 2 * 8 + 2 * 4 + 2 * 6;
 
-template <int D, int BLK>
+template <int D, int BLK, int NS>
 struct PCfg {
+  static_assert(NS == 2 || NS == 3, "slots");
+  static constexpr int NB = NS == 2 ? 2 : 1;              // S buffers per slot
+  static constexpr int NUM_WARPS = 4 * NS + 4;           // softmax WGs, MMA, K, Q, selection
+  static constexpr int NUM_THREADS = NUM_WARPS * 32;
+  static constexpr int WARP_MMA = 4 * NS, WARP_K = 4 * NS + 1, WARP_Q = 4 * NS + 2,
+                       WARP_SEL = 4 * NS + 3;
+  static constexpr int REG_LAUNCH = NS == 2 ? 168 : 128;
+  static constexpr int REG_OTHER = 88;
+  // 208 / 136 (ptxas compiles every role within REG_LAUNCH; the softmax code of NS = 3 fits 128)
+  static constexpr int REG_SOFTMAX = REG_LAUNCH + ((REG_LAUNCH - REG_OTHER) / NS) / 8 * 8;
+  static_assert(NUM_THREADS * REG_LAUNCH <= 65536, "register file");
+  static_assert(4 * NS * (REG_SOFTMAX - REG_LAUNCH) <= 4 * (REG_LAUNCH - REG_OTHER), "pool");
+  static_assert(NS * NB * 128 <= (int)TMEM_COLS, "TMEM");
+  static constexpr int HC = (NS == 2 || BLK <= 64) ? BLK : 64;   // S columns per TMEM read
+  static constexpr int NCH = BLK / HC;                   // reads per pass
   static constexpr int NBOX = D / 64;
   static constexpr int Q_BYTES = BM * D * 2;
   static constexpr int STAGE_BYTES = BLK * D * 2;
@@ -105,13 +74,14 @@ struct PCfg {
   static constexpr int NSEG = BM / SEG;
   // bytes of everything but the Q buffers and the K ring
   static size_t fixed(int g_kv) {
-    return size_t(2) * g_kv * BM * 4 /* block sums */ + size_t(4) * NSEG * g_kv * 4 /* parts */ +
+    return size_t(NS) * g_kv * BM * 4 /* block sums */ +
+           size_t(2 * NS) * NSEG * g_kv * 4 /* partial masses */ +
            size_t((g_kv + 1) & ~1) * 4 /* selection row */ + NBARS * 8 + 16;
   }
-  // (Q buffers, K stages) that fit, preferring 4 Q buffers (both tiles of the next round
-  // prefetched); nst = 0 if nothing fits
+  // (Q buffers, K stages) that fit: one Q buffer per slot plus as many prefetch buffers as fit
+  // (up to one round ahead), then the K ring; nst = 0 if nothing fits
   static void plan(int g_kv, int& nqb, int& nst) {
-    for (nqb = SV_PRED_QB; nqb >= 2; --nqb) {
+    for (nqb = 2 * NS; nqb >= NS; --nqb) {
       const long long left = SMEM_LIMIT - (long long)fixed(g_kv) - (long long)nqb * Q_BYTES;
       nst = left > 0 ? (int)(left / STAGE_BYTES) : 0;
       if (nst > 8) nst = 8;
@@ -124,71 +94,39 @@ struct PCfg {
   }
 };
 
-template <int D, int BLK>
-__global__ void __launch_bounds__(NUM_THREADS, 1)
+template <int D, int BLK, int NS>
+__global__ void __launch_bounds__(PCfg<D, BLK, NS>::NUM_THREADS, 1)
 predict_kernel(const __grid_constant__ CUtensorMap tmap_q,
                const __grid_constant__ CUtensorMap tmap_k, const PredArgs a, int nqb, int nst) {
-  using C = PCfg<D, BLK>;
+  using C = PCfg<D, BLK, NS>;
+  constexpr int NB = C::NB;
   extern __shared__ __align__(1024) uint8_t smem[];
   const int n = a.g_kv;                                  // KV steps of every tile
   uint8_t* sQ = smem;
   uint8_t* sK = smem + nqb * C::Q_BYTES;
-  float* sums = reinterpret_cast<float*>(sK + nst * C::STAGE_BYTES);   // [2][n][BM]
-  float* part = sums + 2 * n * BM;                              // [2 slots][2 bufs][NSEG][n]
-  float* sel_row = part + 4 * C::NSEG * n;                      // [n] selection warp's mass row
+  float* sums = reinterpret_cast<float*>(sK + nst * C::STAGE_BYTES);   // [NS][n][BM]
+  float* part = sums + NS * n * BM;                             // [NS slots][2 bufs][NSEG][n]
+  float* sel_row = part + 2 * NS * C::NSEG * n;                 // [n] selection warp's mass row
   uint64_t* bars = reinterpret_cast<uint64_t*>(sel_row + ((n + 1) & ~1));   // 8-byte aligned
-  uint64_t* q_full = bars;           // [MAXQ]
-  uint64_t* q_empty = q_full + MAXQ; // [MAXQ]
-  uint64_t* kv_full = q_empty + MAXQ;// [8]
-  uint64_t* kv_empty = kv_full + 8;  // [8]
-  uint64_t* s_full = kv_empty + 8;   // [2 slots][2 bufs]
-  uint64_t* s_free = s_full + 4;     // [2 slots][2 bufs] (128 arrivals)
-  uint64_t* part_full = s_free + 4;  // [2 slots][2 bufs] (128 arrivals)
-  uint64_t* part_free = part_full + 4;   // [2 slots][2 bufs]
+  uint64_t* q_full = bars;                 // [MAXQ]
+  uint64_t* q_empty = q_full + MAXQ;       // [MAXQ]
+  uint64_t* kv_full = q_empty + MAXQ;      // [8]
+  uint64_t* kv_empty = kv_full + 8;        // [8]
+  uint64_t* s_full = kv_empty + 8;         // [NS][NB]
+  uint64_t* s_free = s_full + 4;           // [NS][NB] (128 arrivals)
+  uint64_t* part_full = s_free + 4;        // [NS][2] (128 arrivals)
+  uint64_t* part_free = part_full + 6;     // [NS][2]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + NBARS);
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   const int n_tiles = (a.n_q + BM - 1) / BM;
   const int items = n_tiles * a.bh;
-#if SV_PRED_ORDER == 0
-  // contiguous, equal-size range of tiles (every tile costs the same n steps)
+  // contiguous, equal-size range of tiles (every tile costs the same n steps); slot use k runs in
+  // slot k % NS, round k / NS
   const int lo = (int)((long long)items * blockIdx.x / gridDim.x);
   const int hi = (int)((long long)items * (blockIdx.x + 1) / gridDim.x);
   const int T = hi - lo;
-  // global tile (head * n_tiles + tile) of slot use k (slot k & 1, round k >> 1), or -1
-  auto tile_of = [&](int k) -> int { return k < T ? lo + k : -1; };
-#else
-  // Rounds of two tiles (one per slot).  FULL rounds take pairs of adjacent tiles of one (b,h)
-  // (both slots share every K stage), dealt in strided windows: round r of CTA c takes pair
-  // r * grid + (c + rot * r) mod grid, so the grid works on ~grid consecutive pairs at a time (a
-  // few heads, their K_{<=S} L2-resident).  For an odd tile count the last tile of every head is
-  // a SINGLE round (slot 1 idle), dealt one per CTA starting with the CTAs that have one full
-  // round fewer.
-  (void)items;
-  const int fp = n_tiles / 2;
-  const int n_full = fp * a.bh;
-  const int n_single = (n_tiles & 1) ? a.bh : 0;
-  const int grid = gridDim.x;
-  int rot = 59;
-  while (grid > 1 && gcd_pred(rot % grid, grid) != 1) rot += 2;
-  const int k_full = n_full / grid, rem = n_full - k_full * grid;
-  const int pos = (int)((blockIdx.x + (long long)k_full * rot) % grid);
-  const int mine_full = k_full + (pos < rem ? 1 : 0);
-  const int s_first = (pos - rem + grid) % grid;
-  const int mine_single = s_first < n_single ? (n_single - s_first + grid - 1) / grid : 0;
-  const int T = 2 * (mine_full + mine_single);
-  auto tile_of = [&](int k) -> int {
-    const int r = k >> 1, t = k & 1;
-    if (r < mine_full) {
-      const int pr = r * grid + (int)((blockIdx.x + (long long)r * rot) % grid);
-      return (pr / fp) * n_tiles + 2 * (pr % fp) + t;
-    }
-    if (t == 1 || r - mine_full >= mine_single) return -1;
-    const int sg = s_first + (r - mine_full) * grid;
-    return sg * n_tiles + n_tiles - 1;
-  };
-#endif
 
   if (threadIdx.x == 0) {
     if ((smem_u32(smem) & 1023u) != 0) {
@@ -206,14 +144,16 @@ predict_kernel(const __grid_constant__ CUtensorMap tmap_q,
     for (int i = 0; i < 4; ++i) {
       mbar_init(s_full + i, 1);
       mbar_init(s_free + i, BM);
+    }
+    for (int i = 0; i < 6; ++i) {
       mbar_init(part_full + i, BM);
       mbar_init(part_free + i, 1);
     }
     fence_barrier_init();
   }
-  if (warp == WARP_K && lane == 0) prefetch_tmap(&tmap_k);
-  if (warp == WARP_Q && lane == 0) prefetch_tmap(&tmap_q);
-  if (warp == WARP_MMA) {
+  if (warp == C::WARP_K && lane == 0) prefetch_tmap(&tmap_k);
+  if (warp == C::WARP_Q && lane == 0) prefetch_tmap(&tmap_q);
+  if (warp == C::WARP_MMA) {
     tmem_alloc(tmem_slot, TMEM_COLS);
     tmem_relinquish();
   }
@@ -221,22 +161,17 @@ predict_kernel(const __grid_constant__ CUtensorMap tmap_q,
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
-  // slot use k (tile tile_of(k)) runs in slot k & 1, round k >> 1; the valid uses take the Q
-  // buffers in order (the q-th valid one buffer q % nqb).  Both slots of a round start and end
-  // together (equal step counts); a round without slot 1 has tile_of(2r + 1) < 0.
 
-  if (warp >= 8) {
-    reg_dealloc<REG_OTHER>();
-    if (warp == WARP_Q) {
+  if (warp >= 4 * NS) {
+    reg_dealloc<C::REG_OTHER>();
+    if (warp == C::WARP_Q) {
       // ---------------------------------------------------------------- Q loader
+      // use k (tile lo + k) takes Q buffer k % nqb
       if (lane == 0) {
-        int q = 0;
         for (int k = 0; k < T; ++k) {
-          const int it = tile_of(k);
-          if (it < 0) continue;
-          const int b = q % nqb;
-          if (q >= nqb) mbar_wait(q_empty + b, ((q / nqb) - 1) & 1);
-          ++q;
+          const int b = k % nqb;
+          if (k >= nqb) mbar_wait(q_empty + b, ((k / nqb) - 1) & 1);
+          const int it = lo + k;
           mbar_arrive_expect_tx(q_full + b, C::Q_BYTES);
 #pragma unroll
           for (int x = 0; x < C::NBOX; ++x)
@@ -244,45 +179,49 @@ predict_kernel(const __grid_constant__ CUtensorMap tmap_q,
                         (it % n_tiles) * BM, it / n_tiles);
         }
       }
-    } else if (warp == WARP_K) {
+    } else if (warp == C::WARP_K) {
       // ---------------------------------------------------------------- K loader
+      // per round and KV step: one stage per distinct (b,h) among the round's slots, in slot order
       if (lane == 0) {
         const uint64_t pol = policy_evict_last();
-        int idx = 0;
-        for (int r = 0; 2 * r < T; ++r) {
-          const int it0 = tile_of(2 * r), it1 = tile_of(2 * r + 1);
-          const int bh0 = it0 / n_tiles;
-          const bool two = it1 >= 0;
-          const bool shared = two && it1 / n_tiles == bh0;
+        int ring_s = 0;
+        uint32_t ring_ph = 0;
+        for (int k0 = 0; k0 < T; k0 += NS) {
+          int dh[NS], nd = 0;
+#pragma unroll
+          for (int t = 0; t < NS; ++t) {
+            if (k0 + t >= T) break;
+            const int bh = (lo + k0 + t) / n_tiles;
+            bool seen = false;
+            for (int d = 0; d < nd; ++d) seen = seen || dh[d] == bh;
+            if (!seen) dh[nd++] = bh;
+          }
           for (int j = 0; j < n; ++j) {
-            for (int t = 0; t < (two && !shared ? 2 : 1); ++t) {
-              const int bh = (t ? it1 : it0) / n_tiles;
-              const int s = idx % nst;
-              const uint32_t ph = (idx / nst) & 1;
-              ++idx;
-              { PP_T0() mbar_wait(kv_empty + s, ph ^ 1); PP_ADD(3) }
+            for (int d = 0; d < nd; ++d) {
+              const int s = ring_s;
+              mbar_wait(kv_empty + s, ring_ph ^ 1);
+              if (++ring_s == nst) { ring_s = 0; ring_ph ^= 1; }
               mbar_arrive_expect_tx(kv_full + s, C::STAGE_BYTES);
 #pragma unroll
               for (int x = 0; x < C::NBOX; ++x)
                 tma_load_3d_hint(sK + s * C::STAGE_BYTES + x * (BLK * 128), &tmap_k, kv_full + s,
-                                 x * 64, j * BLK, bh, pol);
+                                 x * 64, j * BLK, dh[d], pol);
             }
           }
         }
       }
-    } else if (warp == WARP_SEL) {
+    } else if (warp == C::WARP_SEL) {
       // ---------------------------------------------------------------- selection
-      // Tile k's per-warp partial masses arrive in part[k & 1][(k >> 1) & 1]; this warp sums the
+      // Use k's per-warp partial masses arrive in part[k % NS][(k / NS) & 1]; this warp sums the
       // segments of each query block into its mass row and selects with ballots into bit rows,
       // off the softmax warps' critical path.
       const int W = (n + 31) / 32;
       constexpr int SEG_PER_G = BLK / C::SEG;
       for (int k = 0; k < T; ++k) {
-        const int t = k & 1, kk = k >> 1, pb = kk & 1;
+        const int t = k % NS, kk = k / NS, pb = kk & 1;
         const float* pt = part + (t * 2 + pb) * C::NSEG * n;
-        const int it = tile_of(k);
-        if (it < 0) continue;
         mbar_wait(part_full + 2 * t + pb, (kk >> 1) & 1);
+        const int it = lo + k;
         const int bh = it / n_tiles, tile = it % n_tiles;
         for (int gq = 0; gq < C::G; ++gq) {
           const int u = tile * C::G + gq;
@@ -322,84 +261,101 @@ predict_kernel(const __grid_constant__ CUtensorMap tmap_q,
         }
         if (lane == 0) mbar_arrive(part_free + 2 * t + pb);
       }
-    } else if (warp == WARP_MMA) {
+    } else if (warp == C::WARP_MMA) {
       // ---------------------------------------------------------------- tcgen05 issuer
       constexpr uint32_t IDESC = idesc_bf16_f32(BM, BLK, 0, 0);
       const bool leader = elect_one();
       const uint64_t dq0 = sdesc_sw128(smem_u32(sQ), 16, 1024);
       const uint64_t dk0 = sdesc_sw128(smem_u32(sK), 16, 1024);
-      // ring positions and Q buffer indices as incremental counters: no integer division on the
-      // issue path (the issuer shares its SM sub-partition with two softmax warps)
+      // ring positions and Q-buffer indices as incremental counters: no integer division on the
+      // issue path (the issuer shares its SM sub-partition with softmax warps)
       int ring_s = 0;
       uint32_t ring_ph = 0;
-      int qbuf = 0;                        // Q buffer of slot use k = 2r (round r's first tile)
+      int qbuf = 0;                        // Q buffer of use k0 (the round's first slot)
       uint32_t qph = 0;                    // its use parity
-      uint32_t step0 = 0, step1 = 0;   // S buffer uses per slot
-      PP_T0()
-      for (int r = 0; 2 * r < T; ++r) {
-        const int it0 = tile_of(2 * r), it1 = tile_of(2 * r + 1);
-        const bool two = it1 >= 0;
-        const bool shared = two && it1 / n_tiles == it0 / n_tiles;
-        // Q buffers of the round's tiles (the q-th valid use: buffer q % nqb, parity (q / nqb) & 1)
-        int qb[2];
-        uint32_t qp[2];
-        qb[0] = qbuf;
-        qp[0] = qph;
-        qb[1] = qbuf + 1 == nqb ? 0 : qbuf + 1;
-        qp[1] = qbuf + 1 == nqb ? qph ^ 1 : qph;
-        for (int t = 0; t < (two ? 2 : 1); ++t) {
-          PP_T0() mbar_wait(q_full + qb[t], qp[t]); PP_ADD(2)
+      uint32_t step[NS];                   // S uses per slot
+#pragma unroll
+      for (int t = 0; t < NS; ++t) step[t] = 0;
+      for (int k0 = 0; k0 < T; k0 += NS) {
+        const int ns = min(NS, T - k0);    // slots working this round
+        int qb[NS];
+        bool first_is0[NS], first_self[NS], last_self[NS];   // K-stage sharing (same (b,h))
+        uint32_t qp[NS];
+        {
+          int b = qbuf;
+          uint32_t p = qph;
+#pragma unroll
+          for (int t = 0; t < NS; ++t) {
+            qb[t] = b;
+            qp[t] = p;
+            if (++b == nqb) { b = 0; p ^= 1; }
+          }
         }
-        for (int u = 0; u < (two ? 2 : 1); ++u)
+        {
+          int bhs[NS];
+#pragma unroll
+          for (int t = 0; t < NS; ++t) bhs[t] = t < ns ? (lo + k0 + t) / n_tiles : -1 - t;
+#pragma unroll
+          for (int t = 0; t < NS; ++t) {
+            int first = t;
+#pragma unroll
+            for (int u = t - 1; u >= 0; --u)
+              if (bhs[u] == bhs[t]) first = u;
+            bool later = false;
+#pragma unroll
+            for (int u = t + 1; u < NS; ++u) later = later || bhs[u] == bhs[t];
+            first_self[t] = first == t;
+            first_is0[t] = first == 0;
+            last_self[t] = !later;
+          }
+        }
+        for (int t = 0; t < ns; ++t) mbar_wait(q_full + qb[t], qp[t]);
+        for (int u = 0; u < ns; ++u)
           if (++qbuf == nqb) { qbuf = 0; qph ^= 1; }
         for (int j = 0; j < n; ++j) {
-          int s = 0;
-          for (int t = 0; t < (two ? 2 : 1); ++t) {
-            const uint32_t g = t ? step1 : step0;
-            if (t) ++step1; else ++step0;
-            const int buf = g & 1;
-            // softmax of this slot is done reading S[buf] (step g - 2)
-            { PP_T0() mbar_wait(s_free + 2 * t + buf, ((g >> 1) & 1) ^ 1); PP_ADD(0) }
-            if (t == 0 || !shared) {
-              s = ring_s;
-              { PP_T0() mbar_wait(kv_full + s, ring_ph); PP_ADD(1) }
+          int stg0 = 0, stg1 = 0, stg_t = 0;   // ring stages of slots 0 and 1 this step
+#pragma unroll
+          for (int t = 0; t < NS; ++t) {
+            if (t >= ns) break;
+            const uint32_t g = step[t]++;
+            const int buf = NB == 2 ? int(g & 1) : 0;
+            const uint32_t fpar = (NB == 2 ? (g >> 1) : g) & 1;
+            // the softmax of this slot is done reading this S buffer (use g - NB)
+            mbar_wait(s_free + t * NB + buf, fpar ^ 1);
+            if (first_self[t]) {
+              stg_t = ring_s;
+              mbar_wait(kv_full + ring_s, ring_ph);
               if (++ring_s == nst) { ring_s = 0; ring_ph ^= 1; }
+            } else {
+              stg_t = first_is0[t] ? stg0 : stg1;
             }
+            if (t == 0) stg0 = stg_t;
+            if (t == 1) stg1 = stg_t;
             tc_fence_after();
             const uint64_t da = dq0 + ((uint64_t)(qb[t] * C::Q_BYTES) >> 4);
-            const uint64_t db = dk0 + ((uint64_t)(s * C::STAGE_BYTES) >> 4);
-            {
-            PP_T0()
+            const uint64_t db = dk0 + ((uint64_t)(stg_t * C::STAGE_BYTES) >> 4);
             if (leader) {
 #pragma unroll
               for (int kk = 0; kk < D / 16; ++kk) {
                 const uint32_t oa = ((kk >> 2) * (BM * 128) + (kk & 3) * 32) >> 4;
                 const uint32_t ob = ((kk >> 2) * (BLK * 128) + (kk & 3) * 32) >> 4;
-                mma_ss(tmem + (2 * t + buf) * 128, da + oa, db + ob, IDESC, kk > 0);
+                mma_ss(tmem + (t * NB + buf) * 128, da + oa, db + ob, IDESC, kk > 0);
               }
-              if (t == 1 || !shared || !two) mma_commit(kv_empty + s);
-              mma_commit(s_full + 2 * t + buf);
+              if (last_self[t]) mma_commit(kv_empty + stg_t);
+              mma_commit(s_full + t * NB + buf);
               if (j == n - 1) mma_commit(q_empty + qb[t]);
-            }
-            PP_ADD(8)
-#ifdef SV_PRED_TRACE
-            if (TR_ON && leader && g < 400) {
-              sv_pred_tr_mma[t][g][0] = pp0_;
-              sv_pred_tr_mma[t][g][1] = clock64();
-            }
-#endif
             }
             __syncwarp();
           }
         }
       }
-      PP_ADD(5)
     }
     // no re-grow here: a loader that finished early would race the softmax warps' growth for
     // the CTA's register pool (setmaxnreg.inc blocks), and nothing after this needs registers
   } else {
     // ---------------------------------------------------------------- softmax warpgroups
-    reg_alloc<REG_SOFTMAX>();
+    reg_alloc<C::REG_SOFTMAX>();
+    constexpr int HC = C::HC, NCH = C::NCH;
     const int t = warp >> 2;
     const int quarter = warp & 3;
     const int row = quarter * 32 + lane;
@@ -408,51 +364,79 @@ predict_kernel(const __grid_constant__ CUtensorMap tmap_q,
     const uint64_t sl2x2 = f2_pack(sl2, sl2);
     float* my_sums = sums + t * n * BM;
     uint32_t g = 0;
-#ifdef SV_PRED_PROF
-    const long long ppk_ = clock64();
-#endif
-    for (int k = t; k < T; k += 2) {
-      const int it = tile_of(k);
-      if (it < 0) continue;
+    auto load_chunk = [&](uint32_t col, uint32_t* sr) {
+      if constexpr (HC >= 32) {
+#pragma unroll
+        for (int c = 0; c < HC; c += 32) tmem_ld32(t_row + col + c, sr + c);
+      } else {
+#pragma unroll
+        for (int c = 0; c < HC; c += 8) tmem_ld8(t_row + col + c, sr + c);
+      }
+    };
+    auto mask_chunk = [&](uint32_t* sr, int c0, int valid) {
+      if (__builtin_expect(valid < c0 + HC, 0)) {
+#pragma unroll
+        for (int c = 0; c < HC; ++c)
+          if (c0 + c >= valid) sr[c] = __float_as_uint(-INFINITY);
+      }
+    };
+    auto max_chunk = [&](const uint32_t* sr, float* mm) {
+#pragma unroll
+      for (int c = 0; c < HC; c += 4) {
+        const int q = (c >> 2) & 3;
+        mm[q] = fmax3(mm[q], __uint_as_float(sr[c]), __uint_as_float(sr[c + 1]));
+        mm[q] = fmax3(mm[q], __uint_as_float(sr[c + 2]), __uint_as_float(sr[c + 3]));
+      }
+    };
+    // sum of 2^(s * sl2 - m) over a chunk; column c0 + c of the step picks the emulated pairs
+    auto exp_chunk = [&](const uint32_t* sr, int c0, uint64_t negm, uint64_t* acc, auto emu) {
+      constexpr int E = decltype(emu)::value;
+#pragma unroll
+      for (int c = 0; c < HC; c += 2) {
+        const uint64_t x =
+            ffma2(f2_pack(__uint_as_float(sr[c]), __uint_as_float(sr[c + 1])), sl2x2, negm);
+        float p0, p1;
+        if (E > 0 && ((c0 + c) / 2) % (E > 0 ? E : 1) == E - 1) {
+          ex2_emu2<4>(x, p0, p1);
+        } else {
+          float x0, x1;
+          f2_unpack(x, x0, x1);
+          p0 = ex2(x0);
+          p1 = ex2(x1);
+        }
+        acc[(c >> 1) & 3] = fadd2(acc[(c >> 1) & 3], f2_pack(p0, p1));
+      }
+    };
+    for (int k = t; k < T; k += NS) {
+      const int it = lo + k;
       const int tile = it % n_tiles;
       float m = -INFINITY;
       float l = 0.f;   // running sum of the stored block sums (relative to m)
       for (int j = 0; j < n; ++j, ++g) {
-        const int buf = g & 1;
-        { PP_T0()
-          mbar_wait(s_full + 2 * t + buf, (g >> 1) & 1);
-          if (quarter == 0) { PP_ADD(4) } else { PP_ADD(12) }
-#ifdef SV_PRED_TRACE
-          if (TR_ON && quarter == 0 && lane == 0 && g < 400) sv_pred_tr_sm[t][g][0] = pp0_;
-#endif
-        }
-#ifdef SV_PRED_PROF
-        const long long pps_ = clock64();
-#endif
+        const int buf = NB == 2 ? int(g & 1) : 0;
+        const uint32_t spar = (NB == 2 ? (g >> 1) : g) & 1;
+        const uint32_t s_col = (t * NB + buf) * 128;
+        mbar_wait(s_full + t * NB + buf, spar);
         tc_fence_after();
-        uint32_t sr[BLK];
-        if constexpr (BLK >= 32) {
-#pragma unroll
-          for (int c = 0; c < BLK; c += 32) tmem_ld32(t_row + (2 * t + buf) * 128 + c, sr + c);
-        } else {
-#pragma unroll
-          for (int c = 0; c < BLK; c += 8) tmem_ld8(t_row + (2 * t + buf) * 128 + c, sr + c);
-        }
-        tmem_wait_ld();
-        tc_fence_before();
-        mbar_arrive(s_free + 2 * t + buf);
         const int valid = min(BLK, a.n_kv - j * BLK);   // ragged last KV block (READING 20)
-        if (__builtin_expect(valid < BLK, 0)) {
-#pragma unroll
-          for (int c = 0; c < BLK; ++c)
-            if (c >= valid) sr[c] = __float_as_uint(-INFINITY);
-        }
+        uint32_t sr[HC];
         float mm[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+        if constexpr (NCH == 1) {
+          load_chunk(s_col, sr);
+          tmem_wait_ld();
+          tc_fence_before();
+          mbar_arrive(s_free + t * NB + buf);
+          mask_chunk(sr, 0, valid);
+          max_chunk(sr, mm);
+        } else {
+          // pass 1: the row max over the step, one chunk at a time
 #pragma unroll
-        for (int c = 0; c < BLK; c += 4) {
-          const int q = (c >> 2) & 3;
-          mm[q] = fmax3(mm[q], __uint_as_float(sr[c]), __uint_as_float(sr[c + 1]));
-          mm[q] = fmax3(mm[q], __uint_as_float(sr[c + 2]), __uint_as_float(sr[c + 3]));
+          for (int ch = 0; ch < NCH; ++ch) {
+            load_chunk(s_col + ch * HC, sr);
+            tmem_wait_ld();
+            mask_chunk(sr, ch * HC, valid);
+            max_chunk(sr, mm);
+          }
         }
         const float mx_s = fmax3(fmaxf(mm[0], mm[1]), mm[2], mm[3]) * sl2;
         if (mx_s > m + 8.0f) {
@@ -464,54 +448,39 @@ predict_kernel(const __grid_constant__ CUtensorMap tmap_q,
         }
         const uint64_t negm = f2_pack(-m, -m);
         uint64_t acc[4] = {0, 0, 0, 0};
-        auto exp_sum = [&](auto emu) {
-          constexpr int E = decltype(emu)::value;
-#pragma unroll
-          for (int c = 0; c < BLK; c += 2) {
-            const uint64_t x =
-                ffma2(f2_pack(__uint_as_float(sr[c]), __uint_as_float(sr[c + 1])), sl2x2, negm);
-            float p0, p1;
-            if (E > 0 && (c / 2) % (E > 0 ? E : 1) == E - 1) {
-              ex2_emu2<4>(x, p0, p1);
-            } else {
-              float x0, x1;
-              f2_unpack(x, x0, x1);
-              p0 = ex2(x0);
-              p1 = ex2(x1);
-            }
-            acc[(c >> 1) & 3] = fadd2(acc[(c >> 1) & 3], f2_pack(p0, p1));
-          }
-        };
         // the polynomial exp2 clamps -inf logits to 2^-126, so it only runs on unmasked steps
-        // (warp-uniform branch; masked = the ragged last KV block)
-        if (EMU_EVERY > 0 && __all_sync(0xffffffffu, valid == BLK))
-          exp_sum(std::integral_constant<int, EMU_EVERY>());
-        else
-          exp_sum(std::integral_constant<int, 0>());
+        // (valid depends on j only: CTA-uniform)
+        const bool emu_ok = EMU_EVERY > 0 && valid == BLK;
+        if constexpr (NCH == 1) {
+          if (emu_ok) exp_chunk(sr, 0, negm, acc, std::integral_constant<int, EMU_EVERY>());
+          else exp_chunk(sr, 0, negm, acc, std::integral_constant<int, 0>());
+        } else {
+          // pass 2: exp2 sums; S is released once its last chunk is in registers
+#pragma unroll
+          for (int ch = 0; ch < NCH; ++ch) {
+            load_chunk(s_col + ch * HC, sr);
+            tmem_wait_ld();
+            if (ch == NCH - 1) {
+              tc_fence_before();
+              mbar_arrive(s_free + t * NB + buf);
+            }
+            mask_chunk(sr, ch * HC, valid);
+            if (emu_ok) exp_chunk(sr, ch * HC, negm, acc, std::integral_constant<int, EMU_EVERY>());
+            else exp_chunk(sr, ch * HC, negm, acc, std::integral_constant<int, 0>());
+          }
+        }
         const uint64_t s2 = fadd2(fadd2(acc[0], acc[1]), fadd2(acc[2], acc[3]));
         float s0, s1;
         f2_unpack(s2, s0, s1);
         my_sums[j * BM + row] = s0 + s1;
         l += s0 + s1;
-#ifdef SV_PRED_PROF
-        if (quarter == 0 && lane == 0) { PP_ATOMIC(6, clock64() - pps_) }
-#ifdef SV_PRED_TRACE
-        if (TR_ON && quarter == 0 && lane == 0 && g < 400) {
-          sv_pred_tr_sm[t][g][1] = pps_;
-          sv_pred_tr_sm[t][g][2] = clock64();
-        }
-#endif
-#endif
       }
-#ifdef SV_PRED_PROF
-      const long long ppe_ = clock64();
-#endif
       // ------------------------------------------------------------ tile end: masses
       // P[q, j] = 2^(s' - m) / l: each row's normalised block sums, reduced over the warp's 32
       // rows into part[t][pb][quarter][.] for the selection warp (double-buffered per slot)
       const bool row_valid = tile * BM + row < a.n_q;
       const float inv = row_valid ? 1.f / l : 0.f;
-      const int kk = k >> 1, pb = kk & 1;
+      const int kk = k / NS, pb = kk & 1;
       float* pt = part + (t * 2 + pb) * C::NSEG * n;
       if (kk >= 2) mbar_wait(part_free + 2 * t + pb, ((kk >> 1) - 1) & 1);
       if constexpr (C::SEG == 32) {
@@ -541,25 +510,13 @@ predict_kernel(const __grid_constant__ CUtensorMap tmap_q,
         }
       }
       mbar_arrive(part_full + 2 * t + pb);
-#ifdef SV_PRED_PROF
-      if (quarter == 0 && lane == 0) { PP_ATOMIC(7, clock64() - ppe_) }
-#ifdef SV_PRED_TRACE
-      if (TR_ON && quarter == 0 && lane == 0 && (k >> 1) < 16) {
-        sv_pred_tr_te[t][k >> 1][0] = ppe_;
-        sv_pred_tr_te[t][k >> 1][1] = clock64();
-      }
-#endif
-#endif
     }
-#ifdef SV_PRED_PROF
-    if (quarter == 0 && lane == 0) { PP_ATOMIC(9, clock64() - ppk_) }
-#endif
-    reg_dealloc<REG_LAUNCH>();
+    reg_dealloc<C::REG_LAUNCH>();
   }
 
   tc_fence_before();
   __syncthreads();
-  if (warp == WARP_MMA) {
+  if (warp == C::WARP_MMA) {
     tc_fence_after();
     tmem_dealloc(tmem, TMEM_COLS);
   }
@@ -576,37 +533,62 @@ int num_sms_pred() {
   return n;
 }
 
+// slot count for a shape: three slots when their statistics and one Q buffer per slot fit
 template <int D, int BLK>
-cudaError_t launch_t(const CUtensorMap& tq, const CUtensorMap& tk, const PredArgs& a,
-                     cudaStream_t st) {
-  using C = PCfg<D, BLK>;
+int pick_slots(int g_kv) {
+  int nqb, nst;
+  if (SV_PRED_MAX_SLOTS >= 3) {
+    PCfg<D, BLK, 3>::plan(g_kv, nqb, nst);
+    if (nst >= 2) return 3;
+  }
+  PCfg<D, BLK, 2>::plan(g_kv, nqb, nst);
+  return nst >= 2 ? 2 : 0;
+}
+
+template <int D, int BLK, int NS>
+cudaError_t launch_ns(const CUtensorMap& tq, const CUtensorMap& tk, const PredArgs& a,
+                      cudaStream_t st) {
+  using C = PCfg<D, BLK, NS>;
   int nqb, nst;
   C::plan(a.g_kv, nqb, nst);
   if (nst < 2) return cudaErrorInvalidValue;
   const size_t smem = C::smem(a.g_kv, nqb, nst);
-  auto kern = predict_kernel<D, BLK>;
+  auto kern = predict_kernel<D, BLK, NS>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-#if SV_PRED_ORDER == 0
   const long long items = (long long)((a.n_q + BM - 1) / BM) * a.bh;
-#else
-  const long long items = 2 * (((long long)((a.n_q + BM - 1) / BM) * a.bh + 1) / 2);
-#endif
   if (items <= 0) return cudaSuccess;
   const int sms = num_sms_pred();
-  const int grid = (int)(items >= 2LL * sms ? sms : (items + 1) / 2);
-  kern<<<grid, NUM_THREADS, smem, st>>>(tq, tk, a, nqb, nst);
+  const int grid = (int)(items >= (long long)NS * sms ? sms : (items + NS - 1) / NS);
+  kern<<<grid, C::NUM_THREADS, smem, st>>>(tq, tk, a, nqb, nst);
   return cudaGetLastError();
+}
+
+template <int D, int BLK>
+cudaError_t launch_t(const CUtensorMap& tq, const CUtensorMap& tk, const PredArgs& a,
+                     cudaStream_t st) {
+  const int ns = pick_slots<D, BLK>(a.g_kv);
+  if (ns == 3) return launch_ns<D, BLK, 3>(tq, tk, a, st);
+  if (ns == 2) return launch_ns<D, BLK, 2>(tq, tk, a, st);
+  return cudaErrorInvalidValue;
 }
 
 }  // namespace
 
 size_t predictor_smem_bytes(int head_dim, int block, int g_kv) {
-#define SV_CASE(D_, B_)                            \
-  if (head_dim == D_ && block == B_) {             \
-    int nqb, nst;                                  \
-    PCfg<D_, B_>::plan(g_kv, nqb, nst);            \
-    return nst < 2 ? ~size_t(0) : PCfg<D_, B_>::smem(g_kv, nqb, nst); \
+#define SV_CASE(D_, B_)                                                        \
+  if (head_dim == D_ && block == B_) {                                         \
+    int nqb, nst;                                                              \
+    const int ns = pick_slots<D_, B_>(g_kv);                                   \
+    if (ns == 3) {                                                             \
+      PCfg<D_, B_, 3>::plan(g_kv, nqb, nst);                                   \
+      return PCfg<D_, B_, 3>::smem(g_kv, nqb, nst);                            \
+    }                                                                          \
+    if (ns == 2) {                                                             \
+      PCfg<D_, B_, 2>::plan(g_kv, nqb, nst);                                   \
+      return PCfg<D_, B_, 2>::smem(g_kv, nqb, nst);                            \
+    }                                                                          \
+    return ~size_t(0);                                                         \
   }
   SV_CASE(128, 128) SV_CASE(128, 64) SV_CASE(128, 32) SV_CASE(128, 16)
   SV_CASE(64, 128) SV_CASE(64, 64) SV_CASE(64, 32) SV_CASE(64, 16)
