@@ -533,7 +533,8 @@ int num_sms_pred() {
   return n;
 }
 
-// slot count for a shape: three slots when their statistics and one Q buffer per slot fit
+// slot count for a shape's shared memory: three slots when their statistics and one Q buffer
+// per slot fit (launch_t also requires more than two tiles per SM)
 template <int D, int BLK>
 int pick_slots(int g_kv) {
   int nqb, nst;
@@ -567,7 +568,11 @@ cudaError_t launch_ns(const CUtensorMap& tq, const CUtensorMap& tk, const PredAr
 template <int D, int BLK>
 cudaError_t launch_t(const CUtensorMap& tq, const CUtensorMap& tk, const PredArgs& a,
                      cudaStream_t st) {
-  const int ns = pick_slots<D, BLK>(a.g_kv);
+  // three slots only pay with more than two tiles per SM: a lone three-slot round is ~1.2x
+  // the time of a two-slot round (the third softmax warp shares the sub-partition's MUFU)
+  const long long items = (long long)((a.n_q + BM - 1) / BM) * a.bh;
+  int ns = pick_slots<D, BLK>(a.g_kv);
+  if (ns == 3 && items <= 2LL * num_sms_pred()) ns = 2;
   if (ns == 3) return launch_ns<D, BLK, 3>(tq, tk, a, st);
   if (ns == 2) return launch_ns<D, BLK, 2>(tq, tk, a, st);
   return cudaErrorInvalidValue;

@@ -138,3 +138,34 @@ def test_predict_then_map(sv, cfg):
     dst_b = bits_to_bool(dst.cpu().numpy(), ceil_div(sched.C(K), B))
     for b in range(bh):
         assert (dst_b[b] == map_pattern(src_b[b], sched, S, K, B, cfg["sink"], "footprint")).all()
+
+
+@pytest.mark.parametrize("mode,k,tau", [(0, 5, 0.0), (1, 0, 0.015)])
+def test_predictor_three_slots(sv, mode, k, tau):
+    """The three-slot form (predictor.cu, used above two query tiles per SM): 24 (b,h) at the 2B
+    decision scale = 312 tiles of 128 rows, so every CTA runs full three-slot rounds and the
+    K stages are shared and not shared across slots (13 tiles per (b,h)).  Same protocol as
+    test_predictor_parity: masses (iii) and the strict selection (i) on every unit."""
+    cfg, B, bh = INF2B, 128, 24
+    S = cfg["S"]
+    sched = Schedule(cfg["sides"])
+    q, kc = _struct(cfg, SEED, bh, S)
+    mask, mass = sv.predict_pattern(cfg["sides"], S, B, cfg["sink"], q, kc, mode, max(k, 1), tau)
+    torch.cuda.synchronize()
+    gq, gkv = ceil_div(sched.N(S), B), ceil_div(sched.C(S), B)
+    got_sel = bits_to_bool(mask.cpu().numpy(), gkv)
+    got_mass = mass.cpu().numpy().astype(np.float64)
+    nsb = sink_blocks(sched, cfg["sink"], B)
+    rows = np.array([min((u + 1) * B, sched.N(S)) - u * B for u in range(gq)], dtype=float)
+    for b in range(bh):
+        want_mass = block_mass(to_np(q[b]), to_np(kc[b]), sched, S, B)
+        err = np.abs(got_mass[b] - want_mass)
+        assert (err <= 1e-4 * np.abs(want_mass) + 1e-7 * rows[:, None]).all(), (b, err.max())
+        for u in range(gq):
+            if mode == 0:
+                strict = _select(got_mass[b, u].astype(np.float32).astype(np.float64), mode, k,
+                                 tau, rows[u], nsb)
+            else:
+                strict = got_mass[b, u].astype(np.float32) >= np.float32(tau) * np.float32(rows[u])
+                strict[:nsb] = True
+            assert (strict == got_sel[b, u]).all(), (b, u)
