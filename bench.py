@@ -636,7 +636,7 @@ def main(argv=None):
             "tensor_util_executed": round(exec_tf / peak_tf, 4),
             "csla_attn_ms": round(attn_ms, 4), "dense_attn_ms": round(dense_ms, 4),
             "speedup_vs_dense": round(dense_ms / attn_ms, 3),
-            "predictor": {"kernel": "predict_kernel<128,128> (S = 11, top-5)",
+            "predictor": {"kernel": "predict_kernel<128,128,3> (S = 11, top-5)",
                           "ms": round(pred_ms, 4), "algorithmic_bytes": pred_bytes,
                           "hbm_gbs": round(pred_bytes / (pred_ms * 1e-3) / 1e9, 1),
                           "frac_of_hbm_peak": round(pred_bytes / (pred_ms * 1e-3) / 1e9 / peak_hbm, 4),

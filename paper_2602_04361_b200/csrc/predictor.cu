@@ -34,6 +34,9 @@
 #ifndef SV_PRED_EMU_EVERY
 #define SV_PRED_EMU_EVERY 4   // 1 in 4 exp2 pairs as a degree-4 polynomial on the FMA pipe
 #endif
+#ifndef SV_PRED_STRIDED
+#define SV_PRED_STRIDED 1     // 1: groups of NS tiles dealt round-robin (K L2-resident), 0: ranges
+#endif
 #ifndef SV_PRED_MAX_SLOTS
 #define SV_PRED_MAX_SLOTS 3   // 3: use three slots when shared memory allows, 2: always two
 #endif
@@ -122,11 +125,26 @@ predict_kernel(const __grid_constant__ CUtensorMap tmap_q,
   const int lane = threadIdx.x & 31;
   const int n_tiles = (a.n_q + BM - 1) / BM;
   const int items = n_tiles * a.bh;
-  // contiguous, equal-size range of tiles (every tile costs the same n steps); slot use k runs in
-  // slot k % NS, round k / NS
+  // slot use k runs in slot k % NS, round k / NS; tile_of(k) is its global query tile
+  // (head * n_tiles + tile) or -1 (the valid slots of a round are a prefix)
+#if SV_PRED_STRIDED
+  // groups of NS consecutive tiles dealt round-robin over the CTAs: round r of CTA c takes group
+  // r * grid + c, so at any time the grid works on ~grid * NS consecutive tiles (a few heads,
+  // whose K_{<=S} stays L2-resident and is read from DRAM about once)
+  const int n_groups = (items + NS - 1) / NS;
+  const int rounds = (int)blockIdx.x < n_groups ? (n_groups - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
+  const int T = rounds * NS;
+  auto tile_of = [&](int k) -> int {
+    const int it = ((k / NS) * (int)gridDim.x + (int)blockIdx.x) * NS + k % NS;
+    return it < items ? it : -1;
+  };
+#else
+  // contiguous, equal-size range of tiles (every tile costs the same n steps)
   const int lo = (int)((long long)items * blockIdx.x / gridDim.x);
   const int hi = (int)((long long)items * (blockIdx.x + 1) / gridDim.x);
   const int T = hi - lo;
+  auto tile_of = [&](int k) -> int { return k < T ? lo + k : -1; };
+#endif
 
   if (threadIdx.x == 0) {
     if ((smem_u32(smem) & 1023u) != 0) {
@@ -166,12 +184,15 @@ predict_kernel(const __grid_constant__ CUtensorMap tmap_q,
     reg_dealloc<C::REG_OTHER>();
     if (warp == C::WARP_Q) {
       // ---------------------------------------------------------------- Q loader
-      // use k (tile lo + k) takes Q buffer k % nqb
+      // the q-th valid use takes Q buffer q % nqb
       if (lane == 0) {
+        int q = 0;
         for (int k = 0; k < T; ++k) {
-          const int b = k % nqb;
-          if (k >= nqb) mbar_wait(q_empty + b, ((k / nqb) - 1) & 1);
-          const int it = lo + k;
+          const int it = tile_of(k);
+          if (it < 0) continue;
+          const int b = q % nqb;
+          if (q >= nqb) mbar_wait(q_empty + b, ((q / nqb) - 1) & 1);
+          ++q;
           mbar_arrive_expect_tx(q_full + b, C::Q_BYTES);
 #pragma unroll
           for (int x = 0; x < C::NBOX; ++x)
@@ -190,8 +211,9 @@ predict_kernel(const __grid_constant__ CUtensorMap tmap_q,
           int dh[NS], nd = 0;
 #pragma unroll
           for (int t = 0; t < NS; ++t) {
-            if (k0 + t >= T) break;
-            const int bh = (lo + k0 + t) / n_tiles;
+            const int it = tile_of(k0 + t);
+            if (it < 0) break;
+            const int bh = it / n_tiles;
             bool seen = false;
             for (int d = 0; d < nd; ++d) seen = seen || dh[d] == bh;
             if (!seen) dh[nd++] = bh;
@@ -220,8 +242,9 @@ predict_kernel(const __grid_constant__ CUtensorMap tmap_q,
       for (int k = 0; k < T; ++k) {
         const int t = k % NS, kk = k / NS, pb = kk & 1;
         const float* pt = part + (t * 2 + pb) * C::NSEG * n;
+        const int it = tile_of(k);
+        if (it < 0) continue;
         mbar_wait(part_full + 2 * t + pb, (kk >> 1) & 1);
-        const int it = lo + k;
         const int bh = it / n_tiles, tile = it % n_tiles;
         for (int gq = 0; gq < C::G; ++gq) {
           const int u = tile * C::G + gq;
@@ -277,7 +300,10 @@ predict_kernel(const __grid_constant__ CUtensorMap tmap_q,
 #pragma unroll
       for (int t = 0; t < NS; ++t) step[t] = 0;
       for (int k0 = 0; k0 < T; k0 += NS) {
-        const int ns = min(NS, T - k0);    // slots working this round
+        int ns = 0;                        // slots working this round (a prefix)
+#pragma unroll
+        for (int t = 0; t < NS; ++t)
+          if (tile_of(k0 + t) >= 0) ns = t + 1;
         int qb[NS];
         bool first_is0[NS], first_self[NS], last_self[NS];   // K-stage sharing (same (b,h))
         uint32_t qp[NS];
@@ -294,7 +320,7 @@ predict_kernel(const __grid_constant__ CUtensorMap tmap_q,
         {
           int bhs[NS];
 #pragma unroll
-          for (int t = 0; t < NS; ++t) bhs[t] = t < ns ? (lo + k0 + t) / n_tiles : -1 - t;
+          for (int t = 0; t < NS; ++t) bhs[t] = t < ns ? tile_of(k0 + t) / n_tiles : -1 - t;
 #pragma unroll
           for (int t = 0; t < NS; ++t) {
             int first = t;
@@ -408,7 +434,8 @@ predict_kernel(const __grid_constant__ CUtensorMap tmap_q,
       }
     };
     for (int k = t; k < T; k += NS) {
-      const int it = lo + k;
+      const int it = tile_of(k);
+      if (it < 0) continue;
       const int tile = it % n_tiles;
       float m = -INFINITY;
       float l = 0.f;   // running sum of the stored block sums (relative to m)
