@@ -41,6 +41,19 @@
 #define SV_PRED_MAX_SLOTS 3   // 3: use three slots when shared memory allows, 2: always two
 #endif
 
+#ifdef SV_PRED_TRACE
+// development timeline of one CTA (variant builds only): per slot and S use g, the issuer's
+// s_free-wait start / MMA issue start / issue end and the softmax's s_full-wait start / S seen /
+// step end (warp `quarter 0` of the slot, lane 0)
+__device__ long long sv_ptr[3][320][6];
+extern "C" int sparvar_pred_trace3(long long* out) {
+  return cudaMemcpyFromSymbol(out, sv_ptr, sizeof(sv_ptr)) == cudaSuccess ? 0 : 1;
+}
+#define PTR(t_, g_, i_) if (blockIdx.x == SV_PRED_TRACE && (g_) < 320) sv_ptr[t_][g_][i_] = clock64();
+#else
+#define PTR(t_, g_, i_)
+#endif
+
 namespace sv {
 namespace {
 
@@ -347,6 +360,7 @@ predict_kernel(const __grid_constant__ CUtensorMap tmap_q,
             const int buf = NB == 2 ? int(g & 1) : 0;
             const uint32_t fpar = (NB == 2 ? (g >> 1) : g) & 1;
             // the softmax of this slot is done reading this S buffer (use g - NB)
+            if (lane == 0) { PTR(t, g, 0) }
             mbar_wait(s_free + t * NB + buf, fpar ^ 1);
             if (first_self[t]) {
               stg_t = ring_s;
@@ -361,12 +375,14 @@ predict_kernel(const __grid_constant__ CUtensorMap tmap_q,
             const uint64_t da = dq0 + ((uint64_t)(qb[t] * C::Q_BYTES) >> 4);
             const uint64_t db = dk0 + ((uint64_t)(stg_t * C::STAGE_BYTES) >> 4);
             if (leader) {
+              PTR(t, g, 1)
 #pragma unroll
               for (int kk = 0; kk < D / 16; ++kk) {
                 const uint32_t oa = ((kk >> 2) * (BM * 128) + (kk & 3) * 32) >> 4;
                 const uint32_t ob = ((kk >> 2) * (BLK * 128) + (kk & 3) * 32) >> 4;
                 mma_ss(tmem + (t * NB + buf) * 128, da + oa, db + ob, IDESC, kk > 0);
               }
+              PTR(t, g, 2)
               if (last_self[t]) mma_commit(kv_empty + stg_t);
               mma_commit(s_full + t * NB + buf);
               if (j == n - 1) mma_commit(q_empty + qb[t]);
@@ -443,7 +459,9 @@ predict_kernel(const __grid_constant__ CUtensorMap tmap_q,
         const int buf = NB == 2 ? int(g & 1) : 0;
         const uint32_t spar = (NB == 2 ? (g >> 1) : g) & 1;
         const uint32_t s_col = (t * NB + buf) * 128;
+        if (quarter == 0 && lane == 0) { PTR(t, g, 3) }
         mbar_wait(s_full + t * NB + buf, spar);
+        if (quarter == 0 && lane == 0) { PTR(t, g, 4) }
         tc_fence_after();
         const int valid = min(BLK, a.n_kv - j * BLK);   // ragged last KV block (READING 20)
         uint32_t sr[HC];
@@ -482,12 +500,15 @@ predict_kernel(const __grid_constant__ CUtensorMap tmap_q,
           if (emu_ok) exp_chunk(sr, 0, negm, acc, std::integral_constant<int, EMU_EVERY>());
           else exp_chunk(sr, 0, negm, acc, std::integral_constant<int, 0>());
         } else {
-          // pass 2: exp2 sums; S is released once its last chunk is in registers
+          // pass 2: exp2 sums, starting with the last chunk, still in registers from pass 1;
+          // S is released once the other chunks are in registers
+          if (emu_ok) exp_chunk(sr, (NCH - 1) * HC, negm, acc, std::integral_constant<int, EMU_EVERY>());
+          else exp_chunk(sr, (NCH - 1) * HC, negm, acc, std::integral_constant<int, 0>());
 #pragma unroll
-          for (int ch = 0; ch < NCH; ++ch) {
+          for (int ch = 0; ch < NCH - 1; ++ch) {
             load_chunk(s_col + ch * HC, sr);
             tmem_wait_ld();
-            if (ch == NCH - 1) {
+            if (ch == NCH - 2) {
               tc_fence_before();
               mbar_arrive(s_free + t * NB + buf);
             }
@@ -500,6 +521,7 @@ predict_kernel(const __grid_constant__ CUtensorMap tmap_q,
         float s0, s1;
         f2_unpack(s2, s0, s1);
         my_sums[j * BM + row] = s0 + s1;
+        if (quarter == 0 && lane == 0) { PTR(t, g, 5) }
         l += s0 + s1;
       }
       // ------------------------------------------------------------ tile end: masses
