@@ -169,3 +169,20 @@ def test_predictor_three_slots(sv, mode, k, tau):
                 strict = got_mass[b, u].astype(np.float32) >= np.float32(tau) * np.float32(rows[u])
                 strict[:nsb] = True
             assert (strict == got_sel[b, u]).all(), (b, u)
+
+
+@pytest.mark.parametrize("bh", [24, 4])
+def test_predictor_deterministic_repeats(sv, bh):
+    """Repeat runs are bit-identical (fixed-order reductions, no atomics): 24 (b,h) runs the
+    three-slot form, 4 the two-slot form.  Five launches back to back also exercise the
+    persistent pipelines' barrier phases across launches (a race would show as a mismatch)."""
+    cfg = INF2B
+    q, kc = _struct(cfg, SEED, bh, cfg["S"])
+    runs = []
+    for _ in range(5):
+        mask, mass = sv.predict_pattern(cfg["sides"], cfg["S"], 128, cfg["sink"], q, kc, 0, 5, 0.0)
+        runs.append((mask.clone(), mass.clone()))
+    torch.cuda.synchronize()
+    for mask, mass in runs[1:]:
+        assert torch.equal(mask, runs[0][0])
+        assert torch.equal(mass, runs[0][1])
