@@ -994,12 +994,14 @@ attn_fwd_kernel(const __grid_constant__ CUtensorMap tmap_q,
 #pragma unroll
               for (int c = 0; c < CH / 2; c += 8) tmem_st8(t_row + s_col + c0 / 2 + c, p + c);
             }
+#if !SV_LEAN
             if (BLK >= 64 && c0 + CH == BLK / 2) {
               // first half of P is in TMEM: let the MMA warp start P.V on it
               tmem_wait_st();
               tc_fence_before();
               mbar_arrive(p_bar + 2 * t);
             }
+#endif
           }
           {
             SV_STAMP(5 * (s_cnt - 1) + 3)
@@ -1017,8 +1019,10 @@ attn_fwd_kernel(const __grid_constant__ CUtensorMap tmap_q,
           }
           tmem_wait_st();
           tc_fence_before();
+#if !SV_LEAN
           if (BLK < 64) mbar_arrive(p_bar + 2 * t);
-          mbar_arrive(p_bar + 2 * t + 1);
+#endif
+          mbar_arrive(p_bar + 2 * t + 1);   // the lean issuer waits on this one only
           SV_STAMP(5 * (s_cnt - 1) + 4)
           ++j;
           v = v_n;
