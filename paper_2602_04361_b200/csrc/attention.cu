@@ -919,16 +919,13 @@ attn_fwd_kernel(const __grid_constant__ CUtensorMap tmap_q,
               }
             };
             if constexpr (BLK >= 64) {
-              // two halves: the second half's TMEM load overlaps the first half's max
+              // one batch of TMEM loads for the whole step's S and one wait (two half batches
+              // with the first half's max between them paid two load latencies: 1-3% slower)
 #pragma unroll
-              for (int c = 0; c < BLK / 2; c += 32) tmem_ld32(t_row + s_col + c, sr + c);
-              tmem_wait_ld();
-#pragma unroll
-              for (int c = BLK / 2; c < BLK; c += 32) tmem_ld32(t_row + s_col + c, sr + c);
+              for (int c = 0; c < BLK; c += 32) tmem_ld32(t_row + s_col + c, sr + c);
               have_n = st.next(a, v_n, gm_n);
-              mask_and_max(0, BLK / 2);
               tmem_wait_ld();
-              mask_and_max(BLK / 2, BLK);
+              mask_and_max(0, BLK);
             } else {
               if constexpr (BLK == 32) {
                 tmem_ld32(t_row + s_col, sr);
